@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""TOPLOC prove+verify throughput (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config cfg2] [--impl b200|reference]
+
+One step = prove (tl_select + tl_commit) + verify (tl_verify) of every rollout of
+this rank's batch, inputs resident in HBM (configs[1] = 256 rollouts x 8192
+tokens, hidden 5120, per GPU; weak scaling over ranks).  Rank 0 prints one JSON
+line.  ``--impl reference`` times the CPU TOPLOC restatement (oracle port) on the
+host cores instead (the reference has no TOPLOC code of its own).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TOPLOC tokens/sec (prove+verify) at hidden 5120; % of HBM roofline"
+CONFIGS = {
+    "cfg1": dict(R=1, T=2048, H=1024, name="configs[0]: 1 rollout x 2048 tokens, hidden 1024"),
+    "cfg2": dict(R=256, T=8192, H=5120, name="configs[1]: QwQ-32B shape, 256 rollouts x 8192 tokens, hidden 5120"),
+    "cfg3": dict(R=64, T=32768, H=5120, name="configs[2]: 64 rollouts x 32768 tokens, hidden 5120"),
+    "cfg5": dict(R=1024, T=4096, H=8192, name="configs[4]: Llama-3-70B shape, 1024 rollouts x 4096 tokens, hidden 8192"),
+}
+CHUNK, TOPK = 32, 128
+PROOF_BYTES = 2 + 2 * TOPK
+JITTER_THR = 3277          # 5 % of elements +-1 ulp in the validator's recompute
+LAUNCHES_PER_STEP = 7      # select: prefix+select; commit: inv_table+commit; verify: prefix+verify+verdict
+
+
+def algorithmic_bytes_per_token(H: int) -> float:
+    """prove reads 2H + writes 258/32; verify reads 2H + 258/32."""
+    return 4 * H + 2 * PROOF_BYTES / CHUNK
+
+
+def select_bytes_per_token(H: int) -> float:
+    """tl_select alone: reads 2H per token, writes K x (4 + 2) bytes per 32-token chunk."""
+    return 2 * H + TOPK * 6 / CHUNK
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self._t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU baseline (oracle port)
+def _cpu_worker(args):
+    """One worker = one rollout slice: oracle prove + verify (TOPLOC restatement)."""
+    (T, H, seed, start_evt, q) = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    import numpy as np
+    from oracle import toploc_oracle as TO
+    from oracle.synth_cpu import synth_bits
+    prv = np.concatenate([synth_bits(r, min(512, T - r), H, seed) for r in range(0, T, 512)])
+    val = np.concatenate([synth_bits(r, min(512, T - r), H, seed, jitter_thr=JITTER_THR, jitter_seed=seed + 1)
+                          for r in range(0, T, 512)])
+    offs = [0, T]
+    q.put(("ready", None))
+    start_evt.wait()
+    t0 = time.perf_counter()
+    tab, chunks = TO._chunks_of(prv, offs, CHUNK)
+    _, _, proofs = TO.prove_chunks(chunks, TOPK, batch=16)
+    stats, verdict = TO.verify_proofs(val, offs, [proofs], CHUNK, TOPK)
+    dt = time.perf_counter() - t0
+    q.put(("done", (dt, T, bool(verdict[0]))))
+
+
+def cpu_sample(T: int, H: int, workers: int, steps: int = 1, warmup: int = 0):
+    """Run `warmup + steps` rounds of `workers` parallel oracle prove+verify slices."""
+    ctx = mp.get_context("spawn")
+    results = []
+    for it in range(warmup + steps):
+        q = ctx.Queue()
+        evt = ctx.Event()
+        procs = [ctx.Process(target=_cpu_worker, args=((T, H, 7 + it * 1000 + w, evt, q),)) for w in range(workers)]
+        for p in procs:
+            p.start()
+        for _ in procs:
+            assert q.get()[0] == "ready"
+        t0 = time.perf_counter()
+        evt.set()
+        done = [q.get()[1] for _ in procs]
+        wall = time.perf_counter() - t0
+        for p in procs:
+            p.join()
+        if it >= warmup:
+            results.append((wall, sum(d[1] for d in done), all(d[2] for d in done)))
+    wall = sum(r[0] for r in results)
+    toks = sum(r[1] for r in results)
+    return toks / wall, wall / len(results), all(r[2] for r in results)
+
+
+def cpu_workers() -> int:
+    n = os.cpu_count() or 1
+    try:
+        import psutil
+        mem_gb = psutil.virtual_memory().available / 2 ** 30
+        n = min(n, max(1, int(mem_gb // 2)))
+    except Exception:
+        pass
+    return max(1, min(n, 64))
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    workers = cpu_workers()
+    T_slice = 1024
+    tps, per_step, ok = cpu_sample(T_slice, cfg["H"], workers, steps=args.steps, warmup=args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+        "config": {"workload": cfg["name"], "hidden": cfg["H"], "chunk": CHUNK, "topk": TOPK,
+                   "sample": f"{workers} parallel slices of {T_slice} tokens x H={cfg['H']} per step"},
+        "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": workers, "kind": "port",
+                         "sample": f"{workers} x {T_slice}-token slices (hidden {cfg['H']}) per step, "
+                                   "oracle/toploc_oracle.py prove+verify, one process per core"},
+        "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "all_accepted": ok,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- B200 arm
+def run_b200(args, cfg, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_07291_b200 import api
+    from paper_2505_07291_b200.synth import DISTS, synth_device
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    R, T, H = cfg["R"], cfg["T"], cfg["H"]
+    n_rows = R * T
+    d = DISTS[args.dist]
+    seed = 1000 + rank
+    prv = synth_device(n_rows, H, seed, d, device=dev)
+    val = synth_device(n_rows, H, seed, d, jitter_thr=JITTER_THR, jitter_seed=seed + 1, device=dev)
+    offs = np.arange(R + 1, dtype=np.int64) * T
+    eng = api.engine(dev)
+    plan = eng.plan(offs, H)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        plan.select(prv)
+        plan.commit()
+        plan.verify(val)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # spot-check bit-exactness at full size on sampled chunks (outside the timed region)
+    spot = None
+    if args.spot_check and rank == 0:
+        from oracle import toploc_oracle as TO
+        from oracle.synth_cpu import synth_bits
+        rng = np.random.default_rng(0)
+        js = sorted(rng.choice(plan.n_chunks, size=min(3, plan.n_chunks), replace=False).tolist())
+        got = plan.proofs.cpu().numpy()
+        okp = []
+        for j in js:
+            r0 = (j // (T // CHUNK)) * T + (j % (T // CHUNK)) * CHUNK
+            rows = min(CHUNK, T - (j % (T // CHUNK)) * CHUNK)
+            bits = synth_bits(r0, rows, H, seed, d)
+            _, _, pr = TO.prove_chunks([bits.reshape(-1)], TOPK)
+            okp.append(pr[0] == got[j].tobytes())
+        spot = {"chunks": js, "proofs_bit_exact": all(okp)}
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        e = evs[k]
+        e[0].record(stream)
+        plan.select(prv)
+        e[1].record(stream)
+        plan.commit()
+        e[2].record(stream)
+        plan.verify(val)
+        e[3].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    sel_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    com_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    ver_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+
+    accepted = int(plan.rollout_accept.sum().item())
+    # max over ranks (device-timed)
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    gather_ms = None
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        out = torch.empty(world * R, dtype=torch.uint8, device=dev)
+        g0.record(stream)
+        dist.all_gather_into_tensor(out, plan.rollout_accept)
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        gather_ms = g0.elapsed_time(g1)
+    max_ms = float(t.item())
+    tokens = world * R * T * args.steps
+    value = tokens / (max_ms / 1e3)
+    ms_per_step = max_ms / args.steps
+
+    # e2e through the public API with host buffers (bounded sample of rollouts)
+    e2e = None
+    if args.e2e:
+        Re = min(R, args.e2e_rollouts)
+        rows = Re * T
+        hp = torch.empty((rows, H), dtype=torch.bfloat16).pin_memory()
+        hv = torch.empty((rows, H), dtype=torch.bfloat16).pin_memory()
+        hp.copy_(prv[:rows].cpu())
+        hv.copy_(val[:rows].cpu())
+        offs_e = offs[:Re + 1]
+        times = []
+        h2d = d2h = 0
+        for it in range(1 + args.e2e_steps):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            pb = eng.prove(hp, offs_e)                      # H2D inside the call
+            proofs_host = pb.proofs.cpu()                   # prover ships proofs
+            vb = eng.verify(hv, offs_e, proofs_host)        # validator: H2D hidden + proofs
+            verdict_host = vb.rollout_accept.cpu()
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            if it >= 1:
+                times.append(a.elapsed_time(b))
+            h2d = 2 * rows * H * 2 + proofs_host.numel() + (len(offs_e)) * 8 * 2
+            d2h = proofs_host.numel() + verdict_host.numel()
+        te = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * rows / (float(te.item()) / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "rollouts_per_gpu": Re,
+               "note": "public API (ToplocEngine.prove/verify) from pinned host tensors; proofs and verdicts read back"}
+
+    peak, peak_src = measured_peak()
+    sel_bytes = n_rows * select_bytes_per_token(H)
+    achieved = sel_bytes / (sel_ms / 1e3) / 1e9
+    ver_bytes = n_rows * (2 * H + PROOF_BYTES / CHUNK) + plan.n_chunks * 33 + R
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_select_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                pj = json.load(f)
+            if pj.get("config") == args.config:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+
+    cpu = None
+    if args.cpu_baseline and rank == 0 and world == 1:
+        workers = cpu_workers()
+        tps, wall, ok = cpu_sample(args.cpu_tokens, H, workers, steps=1, warmup=0)
+        cpu = {"value": tps, "unit": "tokens/s", "cores": workers, "kind": "port",
+               "sample": f"{workers} parallel {args.cpu_tokens}-token slices x H={H} "
+                         f"(oracle/toploc_oracle.py prove+verify, one process per core), wall {wall:.1f}s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+            "config": {"workload": cfg["name"], "config": args.config, "rollouts_per_gpu": R, "tokens_per_rollout": T,
+                       "hidden": H, "chunk": CHUNK, "topk": TOPK, "dist": args.dist,
+                       "validator": "same states with 5% of elements +-1 ulp (GPU nondeterminism model)",
+                       "l2": f"inputs {2 * n_rows * H * 2 / 1e9:.1f} GB per GPU >> 126 MB L2; no flush needed",
+                       "parallelism": f"rollout-sharded x{world}"},
+            "roofline": {"bound": "hbm", "kernel": "prove_select_kernel (tl_select)", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": sel_bytes, "avg_launch_ms": sel_ms, "peak_source": peak_src},
+            "step_roofline": {"bytes_per_token": algorithmic_bytes_per_token(H),
+                              "achieved_gbs": value / world * algorithmic_bytes_per_token(H) / 1e9,
+                              "frac": value / world * algorithmic_bytes_per_token(H) / 1e9 / peak},
+            "phases_ms": {"select": sel_ms, "commit": com_ms, "verify": ver_ms,
+                          "verify_gbs": ver_bytes / (ver_ms / 1e3) / 1e9, "verdict_gather": gather_ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "clocks": clk,
+            "rollouts_accepted": f"{accepted}/{R}",
+            "parity_spot_check": spot,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--dist", default="normal", choices=["normal", "massive"])
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--e2e-rollouts", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--cpu-tokens", type=int, default=2048)
+    ap.add_argument("--no-spot-check", dest="spot_check", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":     # rank 0 alone times the CPU path; other ranks exit 0
+        run_reference(args, cfg, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_b200(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,142 @@
+/*
+ * toploc_b200.h -- C ABI of the B200-native TOPLOC rollout-verification path.
+ *
+ * Drop-in boundary.  The reference binds the path by NAME at three Python
+ * import sites (no plugin registry):
+ *   - prove:  swarm/worker/rollout.py:51-68      build_commitments(hidden, k=32)
+ *             called at rollout.py:112 (generate_group) and adversaries.py:312
+ *   - verify: swarm/validator/checks.py:209-213   recompute + digest-list compare
+ *   - wire:   swarm/worker/files.py:37,184-186     commitments[] = ceil(T/k) items
+ * The Python host layer (paper_2505_07291_b200.api / .swarm_adapter) keeps those
+ * names and signatures and calls the entry points below through ctypes; a
+ * ctypes / cffi / pybind binding is all a maintainer of the reference adds
+ * (INTEGRATION.md).
+ *
+ * Conventions
+ *   - every pointer argument is DEVICE memory unless its name ends in _host;
+ *     buffers are caller-owned; the library allocates nothing on the call path;
+ *   - calls are stream-ordered and asynchronous on `stream` (a cudaStream_t,
+ *     NULL = legacy default stream); no host synchronisation inside;
+ *   - return 0 on success or a negative TL_E* code; tl_strerror() names it;
+ *   - the library keeps no mutable global state (safe from many host threads,
+ *     one stream per thread / device).
+ *
+ * Layout
+ *   hidden   : bf16 bit patterns, row-major (n_rows, H), rollouts concatenated
+ *              along rows; row_off[n_roll + 1] (int64) delimits rollout r as rows
+ *              [row_off[r], row_off[r+1]).
+ *   chunk j  : the j-th block of C rows of a rollout (final block partial),
+ *              numbered across rollouts in order; n_chunks = sum ceil(T_r / C).
+ *   proofs   : uint8 [n_chunks][2 + 2K]  (K = 128 -> 258 bytes) :
+ *              modulus p (u16 BE) then coefficients c_0..c_{K-1} (u16 BE).
+ */
+#ifndef TOPLOC_B200_H_
+#define TOPLOC_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TL_OK 0
+#define TL_EINVAL (-1)        /* bad shape / argument                         */
+#define TL_EUNSUPPORTED (-2)  /* K > 128, C*H >= 2^24, ...                     */
+#define TL_EWORKSPACE (-3)    /* workspace too small or misaligned            */
+#define TL_ECUDA (-4)         /* kernel launch / CUDA runtime failure          */
+
+#define TL_MAX_K 128
+#define TL_PROOF_BYTES(K) (2 + 2 * (K))
+
+/* Verdict thresholds; a chunk is accepted iff all three hold (<=). */
+typedef struct tl_thresholds {
+  int32_t max_exp_mismatch;
+  int32_t _pad;
+  double max_mant_mean;
+  double max_mant_median;
+} tl_thresholds;
+
+/* Per-chunk verification statistics (32 bytes). mean/median = +inf when no
+ * exponent matches or the proof is invalid (p < 2). */
+typedef struct tl_chunk_stats {
+  uint32_t exp_mismatch;   /* points whose exponent field differs            */
+  uint32_t n_match;        /* points whose exponent field agrees             */
+  uint32_t mant_sum;       /* sum |mantissa diff| over matching points       */
+  uint32_t flags;          /* bit0 accept, bit1 invalid proof                */
+  double mant_mean;
+  double mant_median;
+} tl_chunk_stats;
+
+#define TL_STAT_ACCEPT 1u
+#define TL_STAT_BADPROOF 2u
+
+const char* tl_strerror(int code);
+int tl_version(void);
+
+/* Host helper: sum_r ceil((row_off_host[r+1]-row_off_host[r]) / C). */
+int64_t tl_count_chunks(const int64_t* row_off_host, int32_t n_roll, int32_t C);
+
+/* Device scratch needed by tl_prove / tl_verify for this problem (bytes). */
+size_t tl_workspace_bytes(int32_t n_roll, int64_t n_chunks, int32_t K);
+
+/*
+ * PROVE (replaces build_commitments at rollout.py:51-68 / :112).
+ * Top-K of every chunk by |bf16| (ties -> lower flat index), GF(p)
+ * interpolation, proof serialisation.  idx_out (int32 [n_chunks][K]) and
+ * bits_out (uint16 [n_chunks][K]) are optional (NULL); entries past
+ * kk = min(K, rows*H) are -1 / 0.
+ */
+int tl_prove(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
+             int32_t H, int32_t C, int32_t K, int64_t n_chunks, uint8_t* proofs_out,
+             int32_t* idx_out, uint16_t* bits_out, void* workspace, size_t workspace_bytes,
+             void* stream);
+
+/*
+ * The two stages of tl_prove, exposed separately (north-star subsystems (a) and
+ * (b)); tl_prove == tl_select + tl_commit on the same stream.
+ *   tl_select: idx_out / bits_out required (int32 / uint16 [n_chunks][K]).
+ *   tl_commit: reads idx / bits as written by tl_select (entries past kk = -1),
+ *              writes proofs_out [n_chunks][2 + 2K].
+ */
+int tl_select(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
+              int32_t H, int32_t C, int32_t K, int64_t n_chunks, int32_t* idx_out,
+              uint16_t* bits_out, void* workspace, size_t workspace_bytes, void* stream);
+int tl_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_t K,
+              uint8_t* proofs_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * VERIFY (replaces the digest compare at checks.py:209-213).
+ * Re-selects top-K on the validator's hidden states, evaluates each proof at
+ * the validator's indices, computes the exponent / mantissa statistics and the
+ * verdicts.  stats_out [n_chunks], chunk_accept_out [n_chunks] (0/1) and
+ * rollout_accept_out [n_roll] (0/1, AND over the rollout's chunks) may be NULL
+ * individually.
+ */
+int tl_verify(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
+              int32_t H, int32_t C, int32_t K, int64_t n_chunks, const uint8_t* proofs,
+              const tl_thresholds* thresholds_host, tl_chunk_stats* stats_out,
+              uint8_t* chunk_accept_out, uint8_t* rollout_accept_out, void* workspace,
+              size_t workspace_bytes, void* stream);
+
+/*
+ * Exact mode (reference parity shim for build_commitments, rollout.py:65):
+ * out[i] = round(in[i], 6) as float64 == rint(x * 1e6) / 1e6 (numpy semantics,
+ * NaN payload kept and quieted).  dtype: 0 f64, 1 f32, 2 bf16, 3 f16.
+ */
+int tl_round6(const void* in, int32_t dtype, int64_t n, double* out, void* stream);
+
+/*
+ * Synthetic bf16 hidden states (bench/test input; counter-based, CPU-replayable,
+ * see paper_2505_07291_b200/synth.py).  normal_table: device uint16[65536].
+ * massive: 6 channel ids (dist 1).  jitter_thr/65536 of elements get +-1 in
+ * the magnitude bits.
+ */
+int tl_synth_bf16(uint16_t* out, int64_t row0, int64_t n_rows, int32_t H, uint64_t seed_mix,
+                  int32_t dist, const uint16_t* normal_table, const int32_t* massive_host,
+                  int32_t jitter_thr, uint64_t jitter_mix, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOPLOC_B200_H_ */

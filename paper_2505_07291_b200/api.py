@@ -1,0 +1,346 @@
+"""Python host API of the TOPLOC prove / verify path (CUDA through the C ABI).
+
+Reference-facing names (the reference binds its path by name, see
+``include/toploc_b200.h``):
+
+* ``build_commitments(hidden, k=32)``  -- exact mode, byte-identical to
+  ``swarm/worker/rollout.py:51-68`` (GPU ``round(x, 6)`` + serialisation, host
+  SHA-256 chain, see ``exact.py``).
+* ``build_proofs(hidden, row_offsets, chunk=32, topk=128)`` -- TOPLOC prove: one
+  258-byte proof per 32-row chunk, ``ceil(T/32)`` per rollout, the same count the
+  rollout-file schema requires for ``commitments`` (``swarm/worker/files.py:184-186``).
+* ``verify_proofs(hidden, row_offsets, proofs, ...)`` -- TOPLOC verify, the
+  replacement of the digest compare at ``swarm/validator/checks.py:209-213``.
+
+``ToplocEngine`` is the device-resident form (inputs and outputs stay in HBM;
+this is what the benchmark times).  There is no CPU fallback: without a CUDA
+device or the in-tree library every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _ffi
+
+CHUNK = 32
+TOPK = 128
+
+STATS_DTYPE = np.dtype([("exp_mismatch", "<u4"), ("n_match", "<u4"), ("mant_sum", "<u4"),
+                        ("flags", "<u4"), ("mant_mean", "<f8"), ("mant_median", "<f8")])
+assert STATS_DTYPE.itemsize == ctypes.sizeof(_ffi.ChunkStats) == 32
+
+
+@dataclass(frozen=True)
+class Thresholds:
+    """Chunk accepted iff exp_mismatch <= max_exp_mismatch, mean <= max_mant_mean and
+    median <= max_mant_median (defaults recalled from the TOPLOC
+    paper -- >= 90 of 128 exponents agree, mean < 10, median < 8 -- unverifiable here)."""
+
+    max_exp_mismatch: int = 38
+    max_mant_mean: float = 10.0
+    max_mant_median: float = 8.0
+
+    def to_c(self) -> _ffi.Thresholds:
+        return _ffi.Thresholds(int(self.max_exp_mismatch), 0, float(self.max_mant_mean),
+                               float(self.max_mant_median))
+
+
+@dataclass
+class VerificationResult:
+    """Per-chunk result (field names follow upstream toploc's VerificationResult)."""
+
+    exp_mismatches: int
+    n_match: int
+    mant_err_sum: int
+    mant_err_mean: float
+    mant_err_median: float
+    accept: bool
+    bad_proof: bool = False
+
+
+def _require_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise RuntimeError("TOPLOC B200 path needs a CUDA device (no CPU fallback)")
+
+
+def _stream_handle(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def as_bf16_bits(hidden, device) -> torch.Tensor:
+    """Accept a bf16 tensor (any device), a uint16 bit array, or a float array/tensor
+    (cast to bf16 RNE) and return a contiguous int16 view on ``device``."""
+    if isinstance(hidden, np.ndarray):
+        if hidden.dtype == np.uint16:
+            t = torch.from_numpy(hidden.view(np.int16))
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(hidden, dtype=np.float32)).to(torch.bfloat16).view(torch.int16)
+    elif isinstance(hidden, torch.Tensor):
+        if hidden.dtype == torch.bfloat16:
+            t = hidden.view(torch.int16)
+        elif hidden.dtype in (torch.int16, torch.uint16):
+            t = hidden.view(torch.int16)
+        else:
+            t = hidden.to(torch.bfloat16).view(torch.int16)
+    else:
+        raise TypeError(f"unsupported hidden type {type(hidden)}")
+    if t.dim() != 2:
+        raise ValueError(f"hidden must be 2-D (rows, H), got shape {tuple(t.shape)}")
+    return t.to(device, non_blocking=True).contiguous()
+
+
+def normalize_offsets(row_offsets, n_rows: int) -> np.ndarray:
+    if row_offsets is None:
+        row_offsets = [0, n_rows]
+    offs = np.asarray(row_offsets.cpu() if isinstance(row_offsets, torch.Tensor) else row_offsets,
+                      dtype=np.int64).reshape(-1)
+    if offs.size < 1 or offs[0] != 0 or offs[-1] != n_rows or np.any(np.diff(offs) < 0):
+        raise ValueError("row_offsets must start at 0, be non-decreasing and end at n_rows")
+    return offs
+
+
+def count_chunks(offs: np.ndarray, chunk: int) -> int:
+    T = np.diff(offs)
+    return int(np.sum((T + chunk - 1) // chunk))
+
+
+@dataclass
+class ProofBatch:
+    proofs: torch.Tensor               # uint8 [n_chunks, 2 + 2K] on device
+    row_offsets: np.ndarray            # host int64 [R + 1]
+    chunk_offsets: np.ndarray          # host int64 [R + 1]: rollout r owns chunks [co[r], co[r+1])
+    indices: torch.Tensor | None = None  # int32 [n_chunks, K]
+    values: torch.Tensor | None = None   # uint16 bits as int16 [n_chunks, K]
+
+    def to_bytes(self) -> list[list[bytes]]:
+        host = self.proofs.cpu().numpy()
+        return [[host[j].tobytes() for j in range(self.chunk_offsets[r], self.chunk_offsets[r + 1])]
+                for r in range(len(self.chunk_offsets) - 1)]
+
+
+@dataclass
+class VerifyBatch:
+    stats: torch.Tensor                # uint8 [n_chunks, 32] (tl_chunk_stats)
+    chunk_accept: torch.Tensor         # uint8 [n_chunks]
+    rollout_accept: torch.Tensor       # uint8 [R]
+    chunk_offsets: np.ndarray = field(default_factory=lambda: np.zeros(1, np.int64))
+
+    def stats_host(self) -> np.ndarray:
+        return self.stats.cpu().numpy().view(STATS_DTYPE).reshape(-1)
+
+    def results(self) -> list[list[VerificationResult]]:
+        st = self.stats_host()
+        out = []
+        for r in range(len(self.chunk_offsets) - 1):
+            out.append([VerificationResult(int(s["exp_mismatch"]), int(s["n_match"]), int(s["mant_sum"]),
+                                           float(s["mant_mean"]), float(s["mant_median"]),
+                                           bool(s["flags"] & _ffi.TL_STAT_ACCEPT),
+                                           bool(s["flags"] & _ffi.TL_STAT_BADPROOF))
+                        for s in st[self.chunk_offsets[r]:self.chunk_offsets[r + 1]]])
+        return out
+
+
+class ToplocEngine:
+    """Device-resident prove / verify on one CUDA device (one host thread per engine)."""
+
+    def __init__(self, device=None, chunk: int = CHUNK, topk: int = TOPK):
+        _require_cuda()
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        self.chunk, self.topk = int(chunk), int(topk)
+        if self.chunk < 1:
+            raise ValueError("interval must be >= 1")
+        if not 1 <= self.topk <= _ffi.TL_MAX_K:
+            raise ValueError(f"topk must be in [1, {_ffi.TL_MAX_K}]")
+        self.lib = _ffi.load()
+        self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self.proof_bytes = 2 + 2 * self.topk
+
+    # ----------------------------------------------------------------- plumbing
+    def _workspace(self, n_roll: int, n_chunks: int) -> torch.Tensor:
+        need = int(self.lib.tl_workspace_bytes(n_roll, n_chunks, self.topk))
+        if self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def _offsets(self, offs: np.ndarray):
+        co = np.zeros(len(offs), dtype=np.int64)
+        T = np.diff(offs)
+        co[1:] = np.cumsum((T + self.chunk - 1) // self.chunk)
+        dev = torch.from_numpy(offs).to(self.device, non_blocking=True)
+        return co, dev
+
+    def plan(self, row_offsets, H: int) -> "Plan":
+        return Plan(self, row_offsets, H)
+
+    # ----------------------------------------------------------------- prove
+    def prove(self, hidden, row_offsets=None, *, return_indices: bool = False,
+              out: torch.Tensor | None = None) -> ProofBatch:
+        h = as_bf16_bits(hidden, self.device)
+        n_rows, H = h.shape
+        offs = normalize_offsets(row_offsets, n_rows)
+        co, offs_dev = self._offsets(offs)
+        n_chunks = int(co[-1])
+        proofs = out if out is not None else torch.empty((n_chunks, self.proof_bytes), dtype=torch.uint8,
+                                                         device=self.device)
+        if proofs.shape != (n_chunks, self.proof_bytes) or proofs.dtype != torch.uint8:
+            raise ValueError("out must be uint8 [n_chunks, 2 + 2K]")
+        idx = vals = None
+        if return_indices:
+            idx = torch.empty((n_chunks, self.topk), dtype=torch.int32, device=self.device)
+            vals = torch.empty((n_chunks, self.topk), dtype=torch.int16, device=self.device)
+        ws = self._workspace(len(offs) - 1, n_chunks)
+        rc = self.lib.tl_prove(h.data_ptr(), offs_dev.data_ptr(), len(offs) - 1, n_rows, H, self.chunk,
+                               self.topk, n_chunks, proofs.data_ptr(), _ptr(idx), _ptr(vals),
+                               ws.data_ptr(), ws.numel(), _stream_handle(self.device))
+        _ffi.check(rc, "tl_prove")
+        return ProofBatch(proofs, offs, co, idx, vals)
+
+    # ----------------------------------------------------------------- verify
+    def verify(self, hidden, row_offsets, proofs, thresholds: Thresholds = Thresholds()) -> VerifyBatch:
+        h = as_bf16_bits(hidden, self.device)
+        n_rows, H = h.shape
+        offs = normalize_offsets(row_offsets, n_rows)
+        co, offs_dev = self._offsets(offs)
+        n_chunks = int(co[-1])
+        pr = self._proof_tensor(proofs, n_chunks)
+        stats = torch.empty((n_chunks, 32), dtype=torch.uint8, device=self.device)
+        cacc = torch.empty(n_chunks, dtype=torch.uint8, device=self.device)
+        racc = torch.empty(len(offs) - 1, dtype=torch.uint8, device=self.device)
+        ws = self._workspace(len(offs) - 1, n_chunks)
+        th = thresholds.to_c()
+        rc = self.lib.tl_verify(h.data_ptr(), offs_dev.data_ptr(), len(offs) - 1, n_rows, H, self.chunk,
+                                self.topk, n_chunks, pr.data_ptr(), ctypes.byref(th), stats.data_ptr(),
+                                cacc.data_ptr(), racc.data_ptr(), ws.data_ptr(), ws.numel(),
+                                _stream_handle(self.device))
+        _ffi.check(rc, "tl_verify")
+        return VerifyBatch(stats, cacc, racc, co)
+
+    def _proof_tensor(self, proofs, n_chunks: int) -> torch.Tensor:
+        if isinstance(proofs, ProofBatch):
+            proofs = proofs.proofs
+        if isinstance(proofs, torch.Tensor):
+            t = proofs.to(self.device).contiguous()
+        else:  # list (per rollout) of list of bytes / hex str, or flat list
+            flat = []
+            for item in proofs:
+                if isinstance(item, (bytes, bytearray, str)):
+                    flat.append(item)
+                else:
+                    flat.extend(item)
+            blobs = [bytes.fromhex(p) if isinstance(p, str) else bytes(p) for p in flat]
+            if any(len(b) != self.proof_bytes for b in blobs):
+                raise ValueError(f"every proof must be {self.proof_bytes} bytes")
+            arr = np.frombuffer(b"".join(blobs), dtype=np.uint8).reshape(-1, self.proof_bytes) \
+                if blobs else np.zeros((0, self.proof_bytes), np.uint8)
+            t = torch.from_numpy(arr.copy()).to(self.device)
+        if t.dtype != torch.uint8 or t.shape != (n_chunks, self.proof_bytes):
+            raise ValueError(f"expected {n_chunks} proofs of {self.proof_bytes} bytes, got {tuple(t.shape)}")
+        return t
+
+
+class Plan:
+    """Pre-allocated device buffers for a fixed batch shape (rollout lengths, H).
+
+    Reusing a plan keeps the hot loop free of allocation and host->device offset
+    copies: ``select`` / ``commit`` / ``prove`` / ``verify`` are one C-ABI call each
+    (the benchmark and the scheduler use this form)."""
+
+    def __init__(self, eng: ToplocEngine, row_offsets, H: int):
+        self.eng = eng
+        self.offs = normalize_offsets(row_offsets, int(np.asarray(row_offsets)[-1]))
+        self.co, self.offs_dev = eng._offsets(self.offs)
+        self.H = int(H)
+        self.n_roll = len(self.offs) - 1
+        self.n_rows = int(self.offs[-1])
+        self.n_chunks = int(self.co[-1])
+        dev, K = eng.device, eng.topk
+        need = int(eng.lib.tl_workspace_bytes(self.n_roll, self.n_chunks, K))
+        self.ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+        self.idx = torch.empty((self.n_chunks, K), dtype=torch.int32, device=dev)
+        self.bits = torch.empty((self.n_chunks, K), dtype=torch.int16, device=dev)
+        self.proofs = torch.empty((self.n_chunks, eng.proof_bytes), dtype=torch.uint8, device=dev)
+        self.stats = torch.empty((self.n_chunks, 32), dtype=torch.uint8, device=dev)
+        self.chunk_accept = torch.empty(self.n_chunks, dtype=torch.uint8, device=dev)
+        self.rollout_accept = torch.empty(self.n_roll, dtype=torch.uint8, device=dev)
+
+    def _check_hidden(self, h: torch.Tensor) -> torch.Tensor:
+        if h.device != self.eng.device or h.shape != (self.n_rows, self.H) or not h.is_contiguous():
+            raise ValueError(f"hidden must be a contiguous ({self.n_rows}, {self.H}) tensor on {self.eng.device}")
+        return h
+
+    def select(self, h: torch.Tensor) -> None:
+        h = self._check_hidden(h)
+        e = self.eng
+        _ffi.check(e.lib.tl_select(h.data_ptr(), self.offs_dev.data_ptr(), self.n_roll, self.n_rows, self.H,
+                                   e.chunk, e.topk, self.n_chunks, self.idx.data_ptr(), self.bits.data_ptr(),
+                                   self.ws.data_ptr(), self.ws.numel(), _stream_handle(e.device)), "tl_select")
+
+    def commit(self) -> None:
+        e = self.eng
+        _ffi.check(e.lib.tl_commit(self.idx.data_ptr(), self.bits.data_ptr(), self.n_chunks, e.topk,
+                                   self.proofs.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                                   _stream_handle(e.device)), "tl_commit")
+
+    def prove(self, h: torch.Tensor) -> torch.Tensor:
+        self.select(h)
+        self.commit()
+        return self.proofs
+
+    def verify(self, h: torch.Tensor, proofs: torch.Tensor | None = None,
+               thresholds: Thresholds = Thresholds()) -> torch.Tensor:
+        h = self._check_hidden(h)
+        e = self.eng
+        pr = self.proofs if proofs is None else proofs
+        th = thresholds.to_c()
+        _ffi.check(e.lib.tl_verify(h.data_ptr(), self.offs_dev.data_ptr(), self.n_roll, self.n_rows, self.H,
+                                   e.chunk, e.topk, self.n_chunks, pr.data_ptr(), ctypes.byref(th),
+                                   self.stats.data_ptr(), self.chunk_accept.data_ptr(),
+                                   self.rollout_accept.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                                   _stream_handle(e.device)), "tl_verify")
+        return self.rollout_accept
+
+
+_ENGINES: dict[tuple, ToplocEngine] = {}
+
+
+def engine(device=None, chunk: int = CHUNK, topk: int = TOPK) -> ToplocEngine:
+    _require_cuda()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    key = (dev.index, chunk, topk)
+    if key not in _ENGINES:
+        _ENGINES[key] = ToplocEngine(dev, chunk, topk)
+    return _ENGINES[key]
+
+
+def build_proofs(hidden, row_offsets=None, chunk: int = CHUNK, topk: int = TOPK, device=None) -> list[list[bytes]]:
+    """TOPLOC prove -> per rollout, ``ceil(T/chunk)`` proofs of ``2 + 2*topk`` bytes."""
+    eng = engine(device, chunk, topk)
+    return eng.prove(hidden, row_offsets).to_bytes()
+
+
+def verify_proofs(hidden, row_offsets, proofs, chunk: int = CHUNK, topk: int = TOPK,
+                  thresholds: Thresholds = Thresholds(), device=None):
+    """TOPLOC verify -> (per-rollout lists of VerificationResult, per-rollout accept)."""
+    eng = engine(device, chunk, topk)
+    vb = eng.verify(hidden, row_offsets, proofs, thresholds)
+    return vb.results(), [bool(v) for v in vb.rollout_accept.cpu().tolist()]
+
+
+def build_commitments(hidden, k: int = CHUNK) -> list[bytes]:
+    """Exact-mode drop-in for ``swarm.worker.rollout.build_commitments`` (rollout.py:51-68)."""
+    from .exact import build_commitments as _bc
+    return _bc(hidden, k)

@@ -1,0 +1,952 @@
+// toploc_b200.cu -- B200 (sm_100a) kernels + C ABI for TOPLOC prove / verify.
+//
+// Path (reference boundary, see include/toploc_b200.h):
+//   prove  = streaming per-chunk top-K select  -> GF(p) commitment  -> 258-B proofs
+//            (replaces swarm/worker/rollout.py:51-68, called at rollout.py:112)
+//   verify = streaming per-chunk top-K select fused with proof evaluation,
+//            exponent/mantissa statistics and verdicts
+//            (replaces swarm/validator/checks.py:209-213)
+// The CPU restatement these kernels are checked against is oracle/toploc_oracle.py
+// (semantics pinned there).
+//
+// HBM roofline: both select kernels read every bf16 of the hidden states exactly
+// once with 128-bit non-allocating loads; the per-element work is a 16x2-SIMD
+// magnitude test against a running per-chunk threshold, so the kernels are
+// HBM-bound.  Only the ~0.1 % of elements that can still enter the top-K take the
+// slow path into a shared-memory candidate buffer.
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "../../include/toploc_b200.h"
+#include "primes.inc"
+
+namespace {
+
+// ----------------------------------------------------------------------------- constants
+constexpr int kSelThreads = 256;              // select CTA
+constexpr int kSelU = 4;                      // 16-B vectors per thread per tile
+constexpr int kSelMinBlocks = 4;              // resident select CTAs per SM (<= 64 regs)
+constexpr int kTileVec = kSelThreads * kSelU; // 1024 vectors = 8192 bf16 per tile
+constexpr int kTileElems = kTileVec * 8;
+constexpr int kCap = 2048;                    // candidate buffer entries (16 KiB)
+constexpr int kRankDirect = 512;              // final select: rank-count threshold
+constexpr unsigned kIdxMask = 0xFFFFFFu;      // flat index field (24 bits)
+constexpr int kInvTables = 8;                 // precomputed inverse tables (first 8 primes)
+constexpr int kCommitWarps = 16;
+constexpr int kCommitThreads = kCommitWarps * 32;
+constexpr uint32_t kPMax = 65497u;
+
+// ----------------------------------------------------------------------------- helpers
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Composite sort key of one element: |bits| (15) | ~idx (24) | bits (16).
+// Descending order == magnitude descending, then flat index ascending.
+__device__ __forceinline__ unsigned long long make_key(unsigned bits, unsigned idx) {
+  return ((unsigned long long)(bits & 0x7FFFu) << 40) |
+         ((unsigned long long)(kIdxMask - idx) << 16) | (unsigned long long)(bits & 0xFFFFu);
+}
+__device__ __forceinline__ unsigned key_idx(unsigned long long s) {
+  return kIdxMask - (unsigned)((s >> 16) & kIdxMask);
+}
+
+struct ModP {
+  uint32_t p, mu;  // mu = floor(2^32 / p), p >= 2
+  __device__ __forceinline__ explicit ModP(uint32_t p_) : p(p_), mu((uint32_t)(0x100000000ull / p_)) {}
+  __device__ __forceinline__ uint32_t red(uint32_t t) const {  // t < 2^32 -> t mod p
+    uint32_t q = __umulhi(t, mu);
+    uint32_t r = t - q * p;
+    return r >= p ? r - p : r;
+  }
+  __device__ __forceinline__ uint32_t mul(uint32_t a, uint32_t b) const { return red(a * b); }
+  __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) const { return a >= b ? a - b : a + p - b; }
+  __device__ __forceinline__ uint32_t add(uint32_t a, uint32_t b) const {
+    uint32_t s = a + b;
+    return s >= p ? s - p : s;
+  }
+  __device__ uint32_t pow(uint32_t a, uint32_t e) const {
+    uint32_t r = 1;
+    while (e) {
+      if (e & 1) r = mul(r, a);
+      a = mul(a, a);
+      e >>= 1;
+    }
+    return r;
+  }
+};
+
+// Chunk j -> (rollout, first row, rows) by binary search over the chunk prefix.
+struct ChunkRef {
+  int64_t row_start;
+  int rows;
+  int rollout;
+};
+__device__ __forceinline__ ChunkRef locate_chunk(const int64_t* __restrict__ prefix,
+                                                 const int64_t* __restrict__ row_off, int n_roll,
+                                                 int64_t j, int C) {
+  int lo = 0, hi = n_roll - 1;  // largest r with prefix[r] <= j
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= j) lo = mid; else hi = mid - 1;
+  }
+  ChunkRef c;
+  c.rollout = lo;
+  const int64_t local = j - prefix[lo];
+  const int64_t T = row_off[lo + 1] - row_off[lo];
+  c.row_start = row_off[lo] + local * C;
+  c.rows = (int)min((int64_t)C, T - local * C);
+  return c;
+}
+
+// ----------------------------------------------------------------------------- streaming select
+struct SelState {
+  unsigned long long buf[kCap];   // candidate keys
+  unsigned long long out[TL_MAX_K];  // selected keys, rank order (also overflow scratch)
+  unsigned long long theta;       // every seen element with key >= theta is in buf
+  unsigned hist[256];
+  int n;                          // candidates appended (may exceed kCap on overflow)
+  int spec;                       // theta is a speculation carried from the previous chunk
+  int delta;                      // speculation margin in magnitude units
+  int digit;
+  int kr;
+  int n_out;
+  // verify-side scratch
+  unsigned p;
+  unsigned mism, nmatch, msum;
+  unsigned mhist[128];
+  uint16_t coef[TL_MAX_K];
+  double median;
+};
+
+__device__ __forceinline__ void append_key(SelState& s, unsigned long long key, int& ovf) {
+  const int pos = atomicAdd(&s.n, 1);
+  if (pos < kCap) s.buf[pos] = key; else ovf = 1;
+}
+
+__device__ __noinline__ void slow8(const uint4 v, unsigned e0, unsigned tkey,
+                                      unsigned long long theta, SelState& s, int& ovf) {
+  const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const unsigned b = (w[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+    if ((b & 0x7FFFu) >= tkey) {
+      const unsigned long long key = make_key(b, e0 + i);
+      if (key >= theta) append_key(s, key, ovf);
+    }
+  }
+}
+
+// k-th largest of buf[0..n) by 8-bit radix select over the 56 significant bits.
+// All threads of the block must call; contains barriers.
+__device__ __noinline__ unsigned long long block_kth_largest(const unsigned long long* buf, int n, int k,
+                                                SelState& s) {
+  unsigned long long prefix = 0, mask = 0;
+  int kr = k;
+  for (int shift = 48; shift >= 0; shift -= 8) {
+    s.hist[threadIdx.x] = 0;  // blockDim == 256 == bins
+    __syncthreads();
+    for (int e = threadIdx.x; e < n; e += kSelThreads) {
+      const unsigned long long v = buf[e];
+      if ((v & mask) == prefix) atomicAdd(&s.hist[(unsigned)(v >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      unsigned c[8], sum = 0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { c[t] = s.hist[255 - (lane * 8 + t)]; sum += c[t]; }
+      unsigned incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      unsigned excl = incl - sum;
+      if ((int)excl < kr && kr <= (int)incl) {
+        unsigned acc = excl;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if ((int)acc < kr && kr <= (int)(acc + c[t])) {
+            s.digit = 255 - (lane * 8 + t);
+            s.kr = kr - (int)acc;
+          }
+          acc += c[t];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= (unsigned long long)s.digit << shift;
+    mask |= 0xFFull << shift;
+    kr = s.kr;
+    __syncthreads();
+  }
+  return prefix;
+}
+
+// Buffer overflowed while processing tile [lo, hi): raise theta to the kk-th largest
+// buffered key (>= kk seen elements are >= it), drop this tile's entries (it is
+// re-processed against the new theta) and everything below theta.
+__device__ __noinline__ void handle_overflow(int lo, int hi, int kk, SelState& s) {
+  const unsigned long long th = block_kth_largest(s.buf, kCap, kk, s);
+  if (threadIdx.x == 0) s.n_out = 0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < kCap; e += kSelThreads) {
+    const unsigned long long v = s.buf[e];
+    const unsigned idx = key_idx(v);
+    if (v >= th && ((int)idx < lo || (int)idx >= hi)) s.out[atomicAdd(&s.n_out, 1)] = v;
+  }
+  __syncthreads();
+  const int nk = s.n_out;
+  for (int e = threadIdx.x; e < nk; e += kSelThreads) s.buf[e] = s.out[e];
+  if (threadIdx.x == 0) {
+    s.n = nk;
+    s.theta = th;
+    s.spec = 0;
+  }
+  __syncthreads();
+}
+
+__device__ __noinline__ void rank_candidates(int kk, SelState& s);
+
+// Top-kk of one chunk (n contiguous bf16 at base) -> s.out[0..kk) in rank order.
+// Entry: s.theta / s.spec hold the threshold speculation for this chunk.
+__device__ void select_chunk(const uint16_t* __restrict__ base, int n, int kk, SelState& s) {
+  const int tid = threadIdx.x;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(base);
+  int a0 = (int)(((16u - (unsigned)(addr & 15u)) & 15u) >> 1);  // scalar head elements
+  if (a0 > n) a0 = n;
+  const int nvec = (n - a0) >> 3;
+  const int tail0 = a0 + (nvec << 3);
+  const int ntiles = max(1, (nvec + kTileVec - 1) / kTileVec);
+  const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(base + a0);
+
+  for (;;) {  // restarts only when a speculative theta proved too high
+    if (tid == 0) s.n = 0;
+    __syncthreads();
+    for (int t = 0; t < ntiles; ++t) {
+      const int lo = (t == 0) ? 0 : a0 + t * kTileElems;
+      const int hi = (t == ntiles - 1) ? n : a0 + (t + 1) * kTileElems;
+      for (;;) {
+        const unsigned long long theta = s.theta;
+        const unsigned tkey = (unsigned)(theta >> 40);
+        const unsigned tidx = key_idx(theta);
+        // elements of this tile tied with theta's magnitude lose on index once lo > tidx
+        const unsigned tk = tkey + ((unsigned)lo > tidx ? 1u : 0u);
+        const unsigned c2 = ((0x8000u - tk) & 0xFFFFu) * 0x10001u;
+        int ovf = 0;
+        uint4 v[kSelU];
+#pragma unroll
+        for (int u = 0; u < kSelU; ++u) {
+          const int g = t * kTileVec + u * kSelThreads + tid;
+          if (g < nvec) v[u] = ld_stream(vb + g);
+        }
+#pragma unroll
+        for (int u = 0; u < kSelU; ++u) {
+          const int g = t * kTileVec + u * kSelThreads + tid;
+          if (g < nvec) {
+            const unsigned m = ((v[u].x & 0x7FFF7FFFu) + c2) | ((v[u].y & 0x7FFF7FFFu) + c2) |
+                               ((v[u].z & 0x7FFF7FFFu) + c2) | ((v[u].w & 0x7FFF7FFFu) + c2);
+            if (m & 0x80008000u) slow8(v[u], (unsigned)(a0 + 8 * g), tkey, theta, s, ovf);
+          }
+        }
+        if (t == 0 && tid < a0) {
+          const unsigned b = base[tid];
+          if ((b & 0x7FFFu) >= tkey) {
+            const unsigned long long key = make_key(b, tid);
+            if (key >= theta) append_key(s, key, ovf);
+          }
+        }
+        if (t == ntiles - 1 && tid < n - tail0) {
+          const unsigned b = base[tail0 + tid];
+          if ((b & 0x7FFFu) >= tkey) {
+            const unsigned long long key = make_key(b, tail0 + tid);
+            if (key >= theta) append_key(s, key, ovf);
+          }
+        }
+        if (!__syncthreads_or(ovf)) break;
+        handle_overflow(lo, hi, kk, s);
+      }
+    }
+    const int nf = s.n;
+    const int spec = s.spec;
+    __syncthreads();
+    if (nf >= kk) break;
+    // speculative theta excluded part of the top-kk: redo the chunk exactly (theta = 0)
+    if (!spec) __trap();  // unreachable: theta = 0 admits every element
+    if (tid == 0) {
+      s.theta = 0;
+      s.spec = 0;
+      s.delta = min(s.delta * 2, 0x4000);
+    }
+    __syncthreads();
+  }
+
+  rank_candidates(kk, s);
+}
+
+// Final ranking of the s.n candidates (keys are unique) into s.out[0..kk), then
+// the threshold speculation for this CTA's next chunk.
+__device__ __noinline__ void rank_candidates(int kk, SelState& s) {
+  const int tid = threadIdx.x;
+  const int nf = s.n;
+  unsigned long long th = 0;
+  if (nf > kRankDirect) th = block_kth_largest(s.buf, nf, kk, s);
+  for (int e = tid; e < nf; e += kSelThreads) {
+    const unsigned long long v = s.buf[e];
+    if (v >= th) {
+      int rank = 0;
+      for (int q = 0; q < nf; ++q) rank += (s.buf[q] > v) ? 1 : 0;
+      if (rank < kk) s.out[rank] = v;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (nf > kk + 256 && s.delta > 1) s.delta >>= 1;
+    const unsigned kmag = (unsigned)(s.out[kk - 1] >> 40);
+    const unsigned d = (unsigned)s.delta;
+    s.theta = kmag > d ? ((unsigned long long)(kmag - d) << 40) : 0ull;
+    s.spec = s.theta != 0ull;
+  }
+}
+
+__device__ __forceinline__ void sel_init(SelState& s) {
+  if (threadIdx.x == 0) {
+    s.theta = 0;
+    s.spec = 0;
+    s.delta = 8;
+  }
+  __syncthreads();
+}
+
+// ----------------------------------------------------------------------------- kernels
+__global__ void chunk_prefix_kernel(const int64_t* __restrict__ row_off, int n_roll, int C,
+                                    int64_t* __restrict__ prefix) {
+  __shared__ int64_t warp_tot[32];
+  __shared__ int64_t carry;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) { carry = 0; prefix[0] = 0; }
+  __syncthreads();
+  for (int base = 0; base < n_roll; base += blockDim.x) {
+    const int r = base + tid;
+    int64_t cnt = 0;
+    if (r < n_roll) {
+      const int64_t T = row_off[r + 1] - row_off[r];
+      cnt = T > 0 ? (T + C - 1) / C : 0;
+    }
+    int64_t incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      int64_t t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xFFFFFFFFu, t, o);
+        if (lane >= o) t += y;
+      }
+      warp_tot[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    const int64_t off = carry + (w ? warp_tot[w - 1] : 0);
+    if (r < n_roll) prefix[r + 1] = off + incl;
+    __syncthreads();
+    if (tid == 0) carry += warp_tot[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kSelThreads, kSelMinBlocks)
+prove_select_kernel(const uint16_t* __restrict__ hidden, const int64_t* __restrict__ row_off,
+                    const int64_t* __restrict__ prefix, int n_roll, int H, int C, int K,
+                    int64_t n_chunks, int32_t* __restrict__ idx_out, uint16_t* __restrict__ bits_out) {
+  __shared__ SelState s;
+  sel_init(s);
+  const int64_t total = prefix[n_roll];
+  for (int64_t j = blockIdx.x; j < n_chunks && j < total; j += gridDim.x) {
+    const ChunkRef cr = locate_chunk(prefix, row_off, n_roll, j, C);
+    const int n = cr.rows * H;
+    const int kk = min(K, n);
+    select_chunk(hidden + cr.row_start * (int64_t)H, n, kk, s);
+    for (int i = threadIdx.x; i < K; i += kSelThreads) {
+      if (i < kk) {
+        const unsigned long long v = s.out[i];
+        idx_out[j * K + i] = (int32_t)key_idx(v);
+        bits_out[j * K + i] = (uint16_t)(v & 0xFFFFu);
+      } else {
+        idx_out[j * K + i] = -1;
+        bits_out[j * K + i] = 0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Warp-wide bitonic sort (ascending over i = lane + 32 r) of 4 registers per lane.
+__device__ __forceinline__ void warp_sort128(uint32_t (&v)[4], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 128; k <<= 1) {
+#pragma unroll
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      if (jj >= 32) {
+        const int rj = jj >> 5;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if ((r & rj) == 0) {
+            const int i = lane + 32 * r;
+            const bool asc = (i & k) == 0;
+            const uint32_t a = v[r], b = v[r | rj];
+            const uint32_t lo = min(a, b), hi = max(a, b);
+            v[r] = asc ? lo : hi;
+            v[r | rj] = asc ? hi : lo;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, v[r], jj);
+          const int i = lane + 32 * r;
+          const bool asc = (i & k) == 0;
+          const bool lower = (lane & jj) == 0;
+          v[r] = (asc == lower) ? min(v[r], o) : max(v[r], o);
+        }
+      }
+    }
+  }
+}
+
+__global__ void inv_table_kernel(uint16_t* __restrict__ tables) {
+  const int q = blockIdx.y;
+  const uint32_t p = kPrimesDesc[q];
+  const ModP m(p);
+  for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < 65536u; a += gridDim.x * blockDim.x)
+    tables[(size_t)q * 65536u + a] = (a == 0 || a >= p) ? 0 : (uint16_t)m.pow(a, p - 2);
+}
+
+// One warp per chunk: modulus search, Newton divided differences over GF(p) with
+// table inverses, Newton -> monomial conversion, 258-byte serialisation.
+__global__ void __launch_bounds__(kCommitThreads, 1)
+commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits, int64_t n_chunks,
+              int K, const uint16_t* __restrict__ inv_tables, uint8_t* __restrict__ proofs) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint16_t* inv0 = reinterpret_cast<uint16_t*>(smem_raw);                  // 65536 x u16
+  uint32_t* xs_all = reinterpret_cast<uint32_t*>(smem_raw + 131072);     // [warps][128]
+  uint32_t* cs_all = xs_all + kCommitWarps * 128;                        // [warps][128]
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(inv_tables);
+    uint4* dst = reinterpret_cast<uint4*>(inv0);
+    for (int i = threadIdx.x; i < 65536 * 2 / 16; i += kCommitThreads) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* xs = xs_all + warp * 128;
+  uint32_t* cs = cs_all + warp * 128;
+  const int PB = 2 + 2 * K;
+
+  for (int64_t j = (int64_t)blockIdx.x * kCommitWarps + warp; j < n_chunks;
+       j += (int64_t)gridDim.x * kCommitWarps) {
+    uint32_t raw[4], yb[4];
+    int kk = 0;
+    uint32_t maxidx = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = lane + 32 * r;
+      int32_t iv = -1;
+      uint32_t b = 0;
+      if (i < K) { iv = idx[j * K + i]; b = bits[j * K + i]; }
+      raw[r] = (uint32_t)iv;
+      yb[r] = b;
+      kk += __popc(__ballot_sync(0xFFFFFFFFu, iv >= 0));
+      if (iv >= 0) maxidx = max(maxidx, (uint32_t)iv);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxidx = max(maxidx, __shfl_xor_sync(0xFFFFFFFFu, maxidx, o));
+
+    // ---- modulus: largest prime with injective residues
+    int pi = 0;
+    uint32_t p = kPMax;
+    if (maxidx >= kPMax) {
+      for (pi = 0; pi < TL_N_PRIMES; ++pi) {
+        p = kPrimesDesc[pi];
+        uint32_t res[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int i = lane + 32 * r;
+          res[r] = (i < kk) ? raw[r] % p : 0x10000u + (uint32_t)i;
+        }
+        warp_sort128(res, lane);
+        bool dup = false;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, res[r], 1);
+          const uint32_t first_next = __shfl_sync(0xFFFFFFFFu, res[r < 3 ? r + 1 : 3], 0);
+          if (lane == 31) nxt = (r < 3) ? first_next : 0xFFFFFFFFu;
+          dup |= (nxt == res[r]);
+        }
+        if (!__any_sync(0xFFFFFFFFu, dup)) break;
+      }
+      if (pi == TL_N_PRIMES) p = 0;
+    }
+    uint8_t* pr = proofs + j * PB;
+    if (p == 0) {  // unprovable chunk: p = 0, zero coefficients
+      for (int b = lane; b < PB; b += 32) pr[b] = 0;
+      continue;
+    }
+    const ModP m(p);
+    const uint16_t* tab = (pi == 0) ? inv0 : (pi < kInvTables ? inv_tables + (size_t)pi * 65536u : nullptr);
+
+    uint32_t x[4], c[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = lane + 32 * r;
+      x[r] = (i < kk) ? m.red(raw[r]) : 0;
+      c[r] = (i < kk) ? m.red(yb[r]) : 0;
+      xs[i] = x[r];
+    }
+    __syncwarp();
+
+    // ---- Newton divided differences: c[i] <- (c[i] - c[i-1]) / (x[i] - x[i-jl])
+    for (int jl = 1; jl < kk; ++jl) {
+      const int r0 = jl >> 5;
+      uint32_t t[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) t[r] = __shfl_sync(0xFFFFFFFFu, c[r], (lane + 31) & 31);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (r < r0) continue;
+        const int i = lane + 32 * r;
+        if (i >= jl && i < kk) {
+          const uint32_t prev = lane ? t[r] : (r ? t[r ? r - 1 : 0] : 0u);
+          const uint32_t d = m.sub(x[r], xs[i - jl]);
+          const uint32_t inv = tab ? (uint32_t)tab[d] : m.pow(d, p - 2);
+          c[r] = m.mul(m.sub(c[r], prev), inv);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) cs[lane + 32 * r] = c[r];
+    __syncwarp();
+
+    // ---- Newton -> monomial: poly <- poly * (X - x_i) + c_i, i = kk-2 .. 0
+    uint32_t poly[4] = {0u, 0u, 0u, 0u};
+    if (lane == 0) poly[0] = cs[kk - 1];
+    for (int i = kk - 2; i >= 0; --i) {
+      const uint32_t xi = xs[i], ci = cs[i];
+      const int deg = kk - 1 - i;
+      uint32_t t[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) t[r] = __shfl_sync(0xFFFFFFFFu, poly[r], (lane + 31) & 31);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (32 * r > deg) continue;
+        const uint32_t prevk = lane ? t[r] : (r ? t[r ? r - 1 : 0] : 0u);
+        uint32_t nv = m.sub(prevk, m.mul(xi, poly[r]));
+        if (lane == 0 && r == 0) nv = m.add(nv, ci);
+        poly[r] = nv;
+      }
+    }
+
+    // ---- serialise: p, c_0..c_{K-1}, u16 big-endian
+    uint16_t* pw = reinterpret_cast<uint16_t*>(pr);
+    if (lane == 0) pw[0] = (uint16_t)(((p & 0xFFu) << 8) | (p >> 8));
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int k = lane + 32 * r;
+      if (k < K) {
+        const uint32_t v = poly[r];
+        pw[1 + k] = (uint16_t)(((v & 0xFFu) << 8) | (v >> 8));
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(kSelThreads, kSelMinBlocks)
+verify_kernel(const uint16_t* __restrict__ hidden, const int64_t* __restrict__ row_off,
+              const int64_t* __restrict__ prefix, int n_roll, int H, int C, int K, int64_t n_chunks,
+              const uint8_t* __restrict__ proofs, tl_thresholds th,
+              tl_chunk_stats* __restrict__ stats_out, uint8_t* __restrict__ accept_out) {
+  __shared__ SelState s;
+  sel_init(s);
+  const int tid = threadIdx.x;
+  const int PB = 2 + 2 * K;
+  const int64_t total = prefix[n_roll];
+  for (int64_t j = blockIdx.x; j < n_chunks && j < total; j += gridDim.x) {
+    const ChunkRef cr = locate_chunk(prefix, row_off, n_roll, j, C);
+    const int n = cr.rows * H;
+    const int kk = min(K, n);
+    select_chunk(hidden + cr.row_start * (int64_t)H, n, kk, s);
+
+    const uint8_t* pr = proofs + j * PB;
+    if (tid == 0) {
+      s.p = ((unsigned)pr[0] << 8) | pr[1];
+      s.mism = 0; s.nmatch = 0; s.msum = 0;
+    }
+    for (int i = tid; i < K; i += kSelThreads) s.coef[i] = (uint16_t)(((unsigned)pr[2 + 2 * i] << 8) | pr[3 + 2 * i]);
+    if (tid < 128) s.mhist[tid] = 0;
+    __syncthreads();
+    const unsigned p = s.p;
+    const bool bad = p < 2;
+    if (!bad && tid < kk) {
+      const ModP m(p);
+      const unsigned long long v = s.out[tid];
+      const uint32_t x = m.red(key_idx(v));
+      const uint32_t obs = m.red((uint32_t)(v & 0xFFFFu));
+      uint32_t acc = 0;
+      for (int k = K - 1; k >= 0; --k) acc = m.red(acc * x + (uint32_t)s.coef[k]);
+      const uint32_t ce = (acc >> 7) & 0xFFu, oe = (obs >> 7) & 0xFFu;
+      if (ce != oe) {
+        atomicAdd(&s.mism, 1u);
+      } else {
+        const int d = abs((int)(acc & 0x7Fu) - (int)(obs & 0x7Fu));
+        atomicAdd(&s.mhist[d], 1u);
+        atomicAdd(&s.msum, (unsigned)d);
+        atomicAdd(&s.nmatch, 1u);
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {  // median over the 128-bin histogram of |mantissa diff|
+      const unsigned nm = s.nmatch;
+      unsigned c4[4], sum = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) { c4[t] = s.mhist[tid * 4 + t]; sum += c4[t]; }
+      unsigned incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (tid >= o) incl += y;
+      }
+      unsigned acc = incl - sum;
+      int v1 = -1, v2 = -1;
+      const unsigned q1 = nm ? (nm - 1) / 2 : 0, q2 = nm / 2;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (acc <= q1 && q1 < acc + c4[t]) v1 = tid * 4 + t;
+        if (acc <= q2 && q2 < acc + c4[t]) v2 = tid * 4 + t;
+        acc += c4[t];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v1 = max(v1, __shfl_xor_sync(0xFFFFFFFFu, v1, o));
+        v2 = max(v2, __shfl_xor_sync(0xFFFFFFFFu, v2, o));
+      }
+      if (tid == 0) {
+        tl_chunk_stats st;
+        if (bad) {
+          st.exp_mismatch = (uint32_t)kk; st.n_match = 0; st.mant_sum = 0;
+          st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
+          st.mant_median = st.mant_mean;
+          st.flags = TL_STAT_BADPROOF;
+        } else {
+          st.exp_mismatch = s.mism; st.n_match = nm; st.mant_sum = s.msum;
+          if (nm) {
+            st.mant_mean = (double)s.msum / (double)nm;
+            st.mant_median = ((double)v1 + (double)v2) * 0.5;
+          } else {
+            st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
+            st.mant_median = st.mant_mean;
+          }
+          const bool acc_ok = (int)st.exp_mismatch <= th.max_exp_mismatch &&
+                              st.mant_mean <= th.max_mant_mean && st.mant_median <= th.max_mant_median;
+          st.flags = acc_ok ? TL_STAT_ACCEPT : 0u;
+        }
+        if (stats_out) stats_out[j] = st;
+        accept_out[j] = (uint8_t)(st.flags & TL_STAT_ACCEPT);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void rollout_verdict_kernel(const uint8_t* __restrict__ chunk_accept,
+                                       const int64_t* __restrict__ prefix, int n_roll,
+                                       uint8_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n_roll) return;
+  int ok = 1;
+  for (int64_t q = prefix[r] + lane; q < prefix[r + 1]; q += 32) ok &= chunk_accept[q] ? 1 : 0;
+  ok = __all_sync(0xFFFFFFFFu, ok);
+  if (lane == 0) out[r] = (uint8_t)ok;
+}
+
+// ----------------------------------------------------------------------------- exact mode
+__device__ __forceinline__ double load_as_f64(const void* in, int dtype, int64_t i) {
+  switch (dtype) {
+    case 0: return reinterpret_cast<const double*>(in)[i];
+    case 1: {
+      const uint32_t b = reinterpret_cast<const uint32_t*>(in)[i];
+      if ((b & 0x7FFFFFFFu) > 0x7F800000u)  // NaN: widen payload like x86 cvtss2sd
+        return __longlong_as_double((long long)(((uint64_t)(b >> 31) << 63) | 0x7FF8000000000000ull |
+                                                ((uint64_t)(b & 0x7FFFFFu) << 29)));
+      return (double)__uint_as_float(b);
+    }
+    case 2: {
+      const uint32_t b = (uint32_t)reinterpret_cast<const uint16_t*>(in)[i] << 16;
+      if ((b & 0x7FFFFFFFu) > 0x7F800000u)
+        return __longlong_as_double((long long)(((uint64_t)(b >> 31) << 63) | 0x7FF8000000000000ull |
+                                                ((uint64_t)(b & 0x7FFFFFu) << 29)));
+      return (double)__uint_as_float(b);
+    }
+    default: {
+      const uint16_t h = reinterpret_cast<const uint16_t*>(in)[i];
+      if ((h & 0x7FFFu) > 0x7C00u)
+        return __longlong_as_double((long long)(((uint64_t)(h >> 15) << 63) | 0x7FF8000000000000ull |
+                                                ((uint64_t)(h & 0x3FFu) << 42)));
+      return (double)__half2float(__ushort_as_half(h));
+    }
+  }
+}
+
+__global__ void round6_kernel(const void* __restrict__ in, int dtype, int64_t n, double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = load_as_f64(in, dtype, i);
+    double r;
+    if (x != x) {  // np.round keeps (and quiets) the NaN payload
+      r = __longlong_as_double(__double_as_longlong(x) | 0x0008000000000000ll);
+    } else {
+      r = __ddiv_rn(rint(__dmul_rn(x, 1e6)), 1e6);
+    }
+    out[i] = r;
+  }
+}
+
+// ----------------------------------------------------------------------------- synthetic input
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct Massive { int c[6]; };
+
+__global__ void synth_kernel(uint16_t* __restrict__ out, int64_t row0, int64_t n_rows, int H,
+                             uint64_t sm, int dist, const uint16_t* __restrict__ table, Massive mv,
+                             int jthr, uint64_t jm) {
+  const int64_t G = (H + 3) / 4;
+  const int64_t total = n_rows * G;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = q / G;
+    const int g = (int)(q - row * G);
+    const uint64_t ctr = (uint64_t)(row0 + row) * (uint64_t)G + (uint64_t)g;
+    const uint64_t z = mix64(ctr + sm);
+    const uint64_t jz = jthr > 0 ? mix64(ctr + jm) : 0ull;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int c = 4 * g + l;
+      if (c >= H) break;
+      uint32_t b;
+      if (dist == 2) b = 0;
+      else if (dist == 3) b = 0x3F80u;
+      else {
+        b = table[(z >> (16 * l)) & 0xFFFFu];
+        if (dist == 1 && (c == mv.c[0] || c == mv.c[1] || c == mv.c[2] || c == mv.c[3] || c == mv.c[4] || c == mv.c[5])) {
+          const float f = __fmul_rn(__uint_as_float(b << 16), 200.0f);
+          b = __bfloat16_as_ushort(__float2bfloat16_rn(f));
+        }
+      }
+      if (jthr > 0) {
+        const uint32_t h = (uint32_t)((jz >> (16 * l)) & 0xFFFFu);
+        if ((int)h < jthr) {
+          uint32_t mag = b & 0x7FFFu;
+          const uint32_t sign = b & 0x8000u;
+          if (h & 1u) { if (mag < 0x7F7Fu) mag += 1; } else { if (mag > 0) mag -= 1; }
+          b = sign | mag;
+        }
+      }
+      out[row * H + c] = (uint16_t)b;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- host helpers
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct WsLayout {
+  size_t prefix, tables, idx, bits, accept, total;
+};
+WsLayout ws_layout(int32_t n_roll, int64_t n_chunks, int32_t K) {
+  WsLayout L;
+  size_t o = 0;
+  L.prefix = o; o = align_up(o + (size_t)(n_roll + 1) * 8, 256);
+  L.tables = o; o = align_up(o + (size_t)kInvTables * 65536 * 2, 256);
+  L.idx = o; o = align_up(o + (size_t)n_chunks * K * 4, 256);
+  L.bits = o; o = align_up(o + (size_t)n_chunks * K * 2, 256);
+  L.accept = o; o = align_up(o + (size_t)n_chunks, 256);
+  L.total = o;
+  return L;
+}
+
+int check_shape(int32_t n_roll, int64_t n_rows, int32_t H, int32_t C, int32_t K, int64_t n_chunks) {
+  if (n_roll < 0 || n_rows < 0 || H < 1 || C < 1 || K < 1 || n_chunks < 0) return TL_EINVAL;
+  if (K > TL_MAX_K) return TL_EUNSUPPORTED;
+  if ((int64_t)C * H >= (int64_t)kIdxMask) return TL_EUNSUPPORTED;
+  return TL_OK;
+}
+
+int sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  return n;
+}
+
+int sel_grid(int64_t n_chunks, const void* kernel) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSelThreads, 0) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const int64_t g = (int64_t)sm_count() * per_sm;
+  return (int)(n_chunks < g ? (n_chunks > 0 ? n_chunks : 1) : g);
+}
+
+int launch_status() { return cudaGetLastError() == cudaSuccess ? TL_OK : TL_ECUDA; }
+
+}  // namespace
+
+// ============================================================================= C ABI
+extern "C" {
+
+const char* tl_strerror(int code) {
+  switch (code) {
+    case TL_OK: return "ok";
+    case TL_EINVAL: return "invalid argument";
+    case TL_EUNSUPPORTED: return "unsupported shape (K in [1,128], C*H < 2^24-1)";
+    case TL_EWORKSPACE: return "workspace too small or misaligned";
+    case TL_ECUDA: return "CUDA launch or runtime failure";
+    default: return "unknown error";
+  }
+}
+
+int tl_version(void) { return 1; }
+
+int64_t tl_count_chunks(const int64_t* row_off_host, int32_t n_roll, int32_t C) {
+  if (!row_off_host || n_roll < 0 || C < 1) return TL_EINVAL;
+  int64_t n = 0;
+  for (int32_t r = 0; r < n_roll; ++r) {
+    const int64_t T = row_off_host[r + 1] - row_off_host[r];
+    if (T < 0) return TL_EINVAL;
+    n += (T + C - 1) / C;
+  }
+  return n;
+}
+
+size_t tl_workspace_bytes(int32_t n_roll, int64_t n_chunks, int32_t K) {
+  return ws_layout(n_roll, n_chunks, K).total;
+}
+
+int tl_select(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
+              int32_t H, int32_t C, int32_t K, int64_t n_chunks, int32_t* idx_out,
+              uint16_t* bits_out, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = check_shape(n_roll, n_rows, H, C, K, n_chunks);
+  if (rc) return rc;
+  if (n_chunks == 0 || n_roll == 0) return TL_OK;
+  if (!hidden || !row_off || !idx_out || !bits_out || !workspace) return TL_EINVAL;
+  const WsLayout L = ws_layout(n_roll, n_chunks, K);
+  if (workspace_bytes < L.total || (reinterpret_cast<uintptr_t>(workspace) & 255)) return TL_EWORKSPACE;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  int64_t* prefix = reinterpret_cast<int64_t*>(ws + L.prefix);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix);
+  prove_select_kernel<<<sel_grid(n_chunks, (const void*)prove_select_kernel), kSelThreads, 0, st>>>(
+      hidden, row_off, prefix, n_roll, H, C, K, n_chunks, idx_out, bits_out);
+  return launch_status();
+}
+
+int tl_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_t K,
+              uint8_t* proofs_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_chunks < 0 || K < 1) return TL_EINVAL;
+  if (K > TL_MAX_K) return TL_EUNSUPPORTED;
+  if (n_chunks == 0) return TL_OK;
+  if (!idx || !bits || !proofs_out || !workspace) return TL_EINVAL;
+  const WsLayout L = ws_layout(0, n_chunks, K);
+  if (workspace_bytes < L.tables + (size_t)kInvTables * 65536 * 2 || (reinterpret_cast<uintptr_t>(workspace) & 255))
+    return TL_EWORKSPACE;
+  uint16_t* tables = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(workspace) + L.tables);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  inv_table_kernel<<<dim3(64, kInvTables), 256, 0, st>>>(tables);
+  const size_t smem = 131072 + 2 * kCommitWarps * 128 * 4;
+  if (cudaFuncSetAttribute(commit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return TL_ECUDA;
+  int grid = sm_count();
+  if ((int64_t)grid * kCommitWarps > n_chunks) grid = (int)((n_chunks + kCommitWarps - 1) / kCommitWarps);
+  commit_kernel<<<grid, kCommitThreads, smem, st>>>(idx, bits, n_chunks, K, tables, proofs_out);
+  return launch_status();
+}
+
+int tl_prove(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
+             int32_t H, int32_t C, int32_t K, int64_t n_chunks, uint8_t* proofs_out,
+             int32_t* idx_out, uint16_t* bits_out, void* workspace, size_t workspace_bytes,
+             void* stream) {
+  int rc = check_shape(n_roll, n_rows, H, C, K, n_chunks);
+  if (rc) return rc;
+  if (n_chunks == 0 || n_roll == 0) return TL_OK;
+  if (!hidden || !row_off || !proofs_out || !workspace) return TL_EINVAL;
+  const WsLayout L = ws_layout(n_roll, n_chunks, K);
+  if (workspace_bytes < L.total || (reinterpret_cast<uintptr_t>(workspace) & 255)) return TL_EWORKSPACE;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  int32_t* idx = idx_out ? idx_out : reinterpret_cast<int32_t*>(ws + L.idx);
+  uint16_t* bits = bits_out ? bits_out : reinterpret_cast<uint16_t*>(ws + L.bits);
+  rc = tl_select(hidden, row_off, n_roll, n_rows, H, C, K, n_chunks, idx, bits, workspace, workspace_bytes, stream);
+  if (rc) return rc;
+  return tl_commit(idx, bits, n_chunks, K, proofs_out, workspace, workspace_bytes, stream);
+}
+
+int tl_verify(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
+              int32_t H, int32_t C, int32_t K, int64_t n_chunks, const uint8_t* proofs,
+              const tl_thresholds* thresholds_host, tl_chunk_stats* stats_out,
+              uint8_t* chunk_accept_out, uint8_t* rollout_accept_out, void* workspace,
+              size_t workspace_bytes, void* stream) {
+  int rc = check_shape(n_roll, n_rows, H, C, K, n_chunks);
+  if (rc) return rc;
+  if (n_roll == 0) return TL_OK;
+  if (!hidden || !row_off || !proofs || !thresholds_host || !workspace) return TL_EINVAL;
+  const WsLayout L = ws_layout(n_roll, n_chunks, K);
+  if (workspace_bytes < L.total || (reinterpret_cast<uintptr_t>(workspace) & 255)) return TL_EWORKSPACE;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  int64_t* prefix = reinterpret_cast<int64_t*>(ws + L.prefix);
+  uint8_t* accept = chunk_accept_out ? chunk_accept_out : ws + L.accept;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+  chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix);
+  if (n_chunks > 0)
+    verify_kernel<<<sel_grid(n_chunks, (const void*)verify_kernel), kSelThreads, 0, st>>>(
+        hidden, row_off, prefix, n_roll, H, C, K, n_chunks, proofs, *thresholds_host, stats_out, accept);
+  if (rollout_accept_out)
+    rollout_verdict_kernel<<<(n_roll + 7) / 8, 256, 0, st>>>(accept, prefix, n_roll, rollout_accept_out);
+  return launch_status();
+}
+
+int tl_round6(const void* in, int32_t dtype, int64_t n, double* out, void* stream) {
+  if (n < 0 || dtype < 0 || dtype > 3) return TL_EINVAL;
+  if (n == 0) return TL_OK;
+  if (!in || !out) return TL_EINVAL;
+  const int64_t blocks = min((int64_t)sm_count() * 8, (n + 255) / 256);
+  round6_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(in, dtype, n, out);
+  return launch_status();
+}
+
+int tl_synth_bf16(uint16_t* out, int64_t row0, int64_t n_rows, int32_t H, uint64_t seed_mix,
+                  int32_t dist, const uint16_t* normal_table, const int32_t* massive_host,
+                  int32_t jitter_thr, uint64_t jitter_mix, void* stream) {
+  if (n_rows < 0 || row0 < 0 || H < 1 || dist < 0 || dist > 3 || jitter_thr < 0) return TL_EINVAL;
+  if (n_rows == 0) return TL_OK;
+  if (!out || ((dist == 0 || dist == 1) && !normal_table)) return TL_EINVAL;
+  Massive mv;
+  for (int i = 0; i < 6; ++i) mv.c[i] = massive_host ? massive_host[i] : -1;
+  const int64_t total = n_rows * ((H + 3) / 4);
+  const int64_t blocks = min((int64_t)sm_count() * 16, (total + 255) / 256);
+  synth_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      out, row0, n_rows, H, seed_mix, dist, normal_table, mv, jitter_thr, jitter_mix);
+  return launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bit-exact bar: top-k indices, value bits, moduli, proof bytes, per-chunk
+exponent-mismatch / match counts / mantissa sums and medians, accept/reject
+verdicts.  The mantissa mean is compared exactly too (it is an exact integer sum
+divided once in float64 on both sides; the north-star tolerance of 1e-6 relative
+is asserted as the weaker bound).
+"""
+
+import hashlib
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import toploc_oracle as TO
+from oracle.synth_cpu import synth_bits
+from paper_2505_07291_b200 import api
+from paper_2505_07291_b200.synth import synth_device
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+MEAN_RTOL = 1e-6
+
+
+def bits_np(t: torch.Tensor) -> np.ndarray:
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def gpu_prove(bits: np.ndarray, offs, K=128, C=32):
+    eng = api.engine(chunk=C, topk=K)
+    pb = eng.prove(torch.from_numpy(bits.view(np.int16)).cuda(), offs, return_indices=True)
+    torch.cuda.synchronize()
+    return pb
+
+
+def check_prove_against_oracle(bits: np.ndarray, offs, K=128, C=32):
+    pb = gpu_prove(bits, offs, K, C)
+    tab, chunks = TO._chunks_of(bits, offs, C)
+    idxs, vals, proofs = TO.prove_chunks(chunks, K)
+    gi = pb.indices.cpu().numpy()
+    gv = pb.values.cpu().numpy().view(np.uint16)
+    gp = pb.proofs.cpu().numpy()
+    assert gp.shape == (len(tab), 2 + 2 * K)
+    for j in range(len(tab)):
+        kk = len(idxs[j])
+        assert np.array_equal(gi[j, :kk], idxs[j]), f"chunk {j} indices"
+        assert np.all(gi[j, kk:] == -1)
+        assert np.array_equal(gv[j, :kk], vals[j]), f"chunk {j} values"
+        assert gp[j].tobytes() == proofs[j], f"chunk {j} proof (p={int.from_bytes(proofs[j][:2], 'big')})"
+    return pb, proofs
+
+
+def stats_tuple(s):
+    return (int(s["exp_mismatch"]), int(s["n_match"]), int(s["mant_sum"]), float(s["mant_median"]),
+            bool(s["flags"] & 1))
+
+
+def check_verify_against_oracle(vbits: np.ndarray, offs, proofs_flat, th=api.Thresholds(), K=128, C=32):
+    eng = api.engine(chunk=C, topk=K)
+    vb = eng.verify(torch.from_numpy(vbits.view(np.int16)).cuda(), offs, proofs_flat, th)
+    torch.cuda.synchronize()
+    st = vb.stats_host()
+    per = []
+    tab = TO.chunk_table(offs, C)
+    it = iter(proofs_flat)
+    per = [[] for _ in range(len(offs) - 1)]
+    for (r, _, _), pr in zip(tab, it):
+        per[r].append(pr)
+    ost, over = TO.verify_proofs(vbits, offs, per, C, K, TO.Thresholds(th.max_exp_mismatch, th.max_mant_mean,
+                                                                         th.max_mant_median))
+    assert len(st) == len(ost)
+    for j, (g, o) in enumerate(zip(st, ost)):
+        assert stats_tuple(g) == (o.exp_mismatch, o.n_match, o.mant_sum, o.mant_median, o.accept), f"chunk {j}"
+        if math.isinf(o.mant_mean):
+            assert math.isinf(g["mant_mean"])
+        else:
+            assert g["mant_mean"] == o.mant_mean
+            assert abs(g["mant_mean"] - o.mant_mean) <= MEAN_RTOL * max(1.0, abs(o.mant_mean))
+    assert [bool(v) for v in vb.rollout_accept.cpu().tolist()] == over
+    assert [bool(v) for v in vb.chunk_accept.cpu().tolist()] == [s.accept for s in ost]
+    return vb, ost, over
+
+
+# ----------------------------------------------------------------------------- synth
+@pytest.mark.parametrize("H,dist,jit", [(1024, 0, 0), (5120, 1, 3277), (1030, 1, 0), (7, 0, 100),
+                                         (256, 2, 3277), (256, 3, 0)])
+def test_synth_device_matches_cpu_twin(H, dist, jit):
+    g = synth_device(70, H, seed=5, dist=dist, row0=33, jitter_thr=jit, jitter_seed=8)
+    torch.cuda.synchronize()
+    c = synth_bits(33, 70, H, 5, dist, jitter_thr=jit, jitter_seed=8)
+    assert np.array_equal(bits_np(g), c)
+
+
+# ----------------------------------------------------------------------------- prove
+def golden_cases():
+    with open(os.path.join(GOLDEN, "toploc_golden.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("case", golden_cases(), ids=lambda c: c["name"])
+def test_prove_and_verify_golden(case):
+    offs, H = case["row_offsets"], case["H"]
+    bits = synth_bits(0, offs[-1], H, case["seed"], case["dist"])
+    pb = gpu_prove(bits, offs, case["K"], case["C"])
+    gp = pb.proofs.cpu().numpy()
+    assert hashlib.sha256(gp.tobytes()).hexdigest() == case["proofs_sha256"]
+    assert gp[0].tobytes().hex() == case["first_proof"]
+    assert list(pb.indices[0, :len(case["first_idx"])].cpu().numpy()) == case["first_idx"]
+    jit = synth_bits(0, offs[-1], H, case["seed"], case["dist"], jitter_thr=case["jitter_thr"],
+                     jitter_seed=case["jitter_seed"])
+    eng = api.engine(chunk=case["C"], topk=case["K"])
+    vb = eng.verify(torch.from_numpy(jit.view(np.int16)).cuda(), offs, pb)
+    st = vb.stats_host()
+    assert [list(stats_tuple(s)) for s in st] == case["jitter_stats"]
+    assert [bool(v) for v in vb.rollout_accept.cpu().tolist()] == case["jitter_verdict"]
+    other = synth_bits(0, offs[-1], H, case["seed"] + 1, 0)
+    vb = eng.verify(torch.from_numpy(other.view(np.int16)).cuda(), offs, pb)
+    assert [list(stats_tuple(s)) for s in vb.stats_host()] == case["wrong_stats"]
+    assert [bool(v) for v in vb.rollout_accept.cpu().tolist()] == case["wrong_verdict"]
+
+
+@pytest.mark.parametrize("H,offs", [
+    (1024, [0, 2048]),                     # configuration 1
+    (5120, [0, 96, 96 + 45]),              # ragged, H of the north star
+    (8192, [0, 64]),                       # configuration 5 hidden
+    (3, [0, 1, 33, 34]),                   # chunks smaller than K
+    (17, [0, 100]),                        # odd H: unaligned chunk starts
+    (2047, [0, 64]),                       # idx just above 65497
+])
+def test_prove_matches_oracle_shapes(H, offs):
+    bits = synth_bits(0, offs[-1], H, seed=H, dist=0)
+    check_prove_against_oracle(bits, offs)
+
+
+def test_prove_many_chunks_mixed_distributions():
+    """More chunks than resident CTAs so every CTA carries its threshold speculation
+    across normal, massive-activation, all-zero and all-equal chunks (speculation
+    failures, overflow re-processing and tie resolution across tiles)."""
+    H, C = 1024, 32
+    n_chunks = 2400
+    parts = []
+    for j in range(n_chunks):
+        d = [0, 1, 2, 3, 0, 1][j % 6] if j % 7 else 2
+        parts.append(synth_bits(j * C, C, H, seed=j % 5, dist=d))
+    bits = np.concatenate(parts)
+    bits[5 * C + 3, 100] = 0x7FC0      # NaN
+    bits[11 * C, 7] = 0xFF80           # -inf
+    bits[13 * C + 31, H - 1] = 0x0001  # denormal
+    offs = list(range(0, n_chunks * C + 1, C * 48))
+    check_prove_against_oracle(bits, offs)
+
+
+def test_prove_collisions_use_fallback_primes():
+    H = 5120
+    bits = synth_bits(0, 32 * 60, H, seed=5, dist=0)
+    _, proofs = check_prove_against_oracle(bits, [0, 32 * 60])
+    assert any(int.from_bytes(p[:2], "big") != 65497 for p in proofs)
+
+
+# ----------------------------------------------------------------------------- verify
+def flat_proofs(pb):
+    return [bytes(b) for b in pb.proofs.cpu().numpy()]
+
+
+@pytest.mark.parametrize("H", [1024, 5120])
+def test_verify_variants_match_oracle(H):
+    offs = [0, 64, 96, 160]
+    bits = synth_bits(0, offs[-1], H, seed=21, dist=1)
+    pb = gpu_prove(bits, offs)
+    pf = flat_proofs(pb)
+    t = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.bfloat16)
+    variants = {
+        "identical": bits,
+        "jitter": synth_bits(0, offs[-1], H, 21, 1, jitter_thr=3277, jitter_seed=4),
+        "fp8": bits_np(t.to(torch.float8_e4m3fn).to(torch.bfloat16)),
+        "scaled_row": bits.copy(),
+        "tampered_row": bits.copy(),
+        "swapped_chunks": bits.copy(),
+        "zeros_chunk": bits.copy(),
+        "other_model": synth_bits(0, offs[-1], H, 99, 1),
+    }
+    v = variants
+    v["scaled_row"][40] = bits_np((t[40].float() * 1.5).to(torch.bfloat16).view(1, -1))[0]
+    v["tampered_row"][70] = synth_bits(1000, 1, H, 3, 0)[0]
+    v["swapped_chunks"][0:32], v["swapped_chunks"][32:64] = bits[32:64].copy(), bits[0:32].copy()
+    v["zeros_chunk"][96:128] = 0
+    for th in (api.Thresholds(), api.Thresholds(8, 2.0, 1.0), api.Thresholds(0, 0.0, 0.0)):
+        for name, vb in v.items():
+            check_verify_against_oracle(vb, offs, pf, th)
+
+
+def test_verify_identical_accepts_and_wrong_rejects():
+    offs = [0, 128, 256]
+    bits = synth_bits(0, 256, 1024, seed=1, dist=0)
+    pb = gpu_prove(bits, offs)
+    eng = api.engine()
+    vb = eng.verify(torch.from_numpy(bits.view(np.int16)).cuda(), offs, pb)
+    assert vb.rollout_accept.cpu().tolist() == [1, 1]
+    st = vb.stats_host()
+    assert np.all(st["exp_mismatch"] == 0) and np.all(st["mant_sum"] == 0)
+    other = synth_bits(0, 256, 1024, seed=2, dist=0)
+    vb = eng.verify(torch.from_numpy(other.view(np.int16)).cuda(), offs, pb)
+    assert vb.rollout_accept.cpu().tolist() == [0, 0]
+
+
+def test_verify_malformed_proofs():
+    offs = [0, 96]
+    H = 640
+    bits = synth_bits(0, 96, H, seed=3, dist=0)
+    pf = flat_proofs(gpu_prove(bits, offs))
+    bad = list(pf)
+    bad[0] = b"\x00\x00" + pf[0][2:]                       # p = 0
+    bad[1] = b"\x00\x01" + pf[1][2:]                       # p = 1
+    bad[2] = pf[2][:2] + b"\xff\xff" * 128                  # coefficients >= p
+    check_verify_against_oracle(bits, offs, bad)
+    bad2 = list(pf)
+    bad2[0] = b"\xff\xff" + pf[0][2:]                      # p = 65535 (composite)
+    check_verify_against_oracle(bits, offs, bad2)
+
+
+def test_api_argument_errors():
+    eng = api.engine()
+    x = torch.zeros((64, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):
+        eng.prove(x, [0, 65])
+    with pytest.raises(ValueError):
+        eng.verify(x, [0, 64], [b"\x00" * 257, b"\x00" * 258])
+    with pytest.raises(ValueError):
+        api.ToplocEngine(topk=129)
+    with pytest.raises(ValueError):
+        api.ToplocEngine(chunk=0)
