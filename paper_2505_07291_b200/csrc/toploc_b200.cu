@@ -31,8 +31,9 @@ constexpr int kSelU = 4;                      // 16-B vectors per thread per til
 constexpr int kSelMinBlocks = 4;              // resident select CTAs per SM (<= 64 regs)
 constexpr int kTileVec = kSelThreads * kSelU; // 1024 vectors = 8192 bf16 per tile
 constexpr int kTileElems = kTileVec * 8;
-constexpr int kCap = 2048;                    // candidate buffer entries (16 KiB)
-constexpr int kRankDirect = 512;              // final select: rank-count threshold
+constexpr int kSelWarps = kSelThreads / 32;
+constexpr int kWarpCap = 256;                 // per-warp candidate buffer (2 KiB)
+constexpr int kStageVec = 32 * kSelU;         // per-warp staging: every vector of one iteration
 constexpr unsigned kIdxMask = 0xFFFFFFu;      // flat index field (24 bits)
 constexpr int kInvTables = 8;                 // precomputed inverse tables (first 8 primes)
 constexpr int kCommitWarps = 16;
@@ -107,14 +108,28 @@ __device__ __forceinline__ ChunkRef locate_chunk(const int64_t* __restrict__ pre
 }
 
 // ----------------------------------------------------------------------------- streaming select
+//
+// One CTA owns one chunk at a time (persistent over chunks).  Each warp streams an
+// interleaved share of the chunk's 16-byte vectors and keeps its own candidate
+// buffer and threshold theta_w with the invariant
+//     every element this warp has seen with key >= theta_w is in its buffer,
+// and, once theta_w was raised by a compaction, >= kk seen elements are >= theta_w.
+// The union of the warp buffers therefore contains the chunk's top-kk (an element
+// below its warp's theta_w is beaten by kk others).  No block barrier is needed
+// while streaming; the chunk ends with one barrier and a warp bitonic sort.
+//
+// The chunk starts from a speculative theta (the previous chunk's kk-th magnitude
+// minus an adaptive margin).  If the union ends with < kk entries the speculation
+// was too high and the chunk is redone from theta = 0 (L2-resident re-read).
 struct SelState {
-  unsigned long long buf[kCap];   // candidate keys
-  unsigned long long out[TL_MAX_K];  // selected keys, rank order (also overflow scratch)
-  unsigned long long theta;       // every seen element with key >= theta is in buf
+  unsigned long long wbuf[kSelWarps][kWarpCap];  // per-warp candidate keys
+  uint4 stage[kSelWarps][kStageVec];             // per-warp flagged vectors
+  int sidx[kSelWarps][kStageVec];                // their vector index
+  unsigned long long out[TL_MAX_K];              // selected keys, rank order
+  unsigned long long theta;                      // chunk-start threshold (speculation)
+  int wcnt[kSelWarps];
   unsigned hist[256];
-  int n;                          // candidates appended (may exceed kCap on overflow)
-  int spec;                       // theta is a speculation carried from the previous chunk
-  int delta;                      // speculation margin in magnitude units
+  int delta;                                     // speculation margin, magnitude units
   int digit;
   int kr;
   int n_out;
@@ -123,31 +138,91 @@ struct SelState {
   unsigned mism, nmatch, msum;
   unsigned mhist[128];
   uint16_t coef[TL_MAX_K];
-  double median;
 };
 
-__device__ __forceinline__ void append_key(SelState& s, unsigned long long key, int& ovf) {
-  const int pos = atomicAdd(&s.n, 1);
-  if (pos < kCap) s.buf[pos] = key; else ovf = 1;
+__device__ __forceinline__ unsigned hmaxabs2(unsigned a, unsigned b) {
+  unsigned d;  // per bf16 half: max(|a|, |b|) (sign = xor, masked off by the caller); NaN wins
+  asm("max.NaN.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ bool coarse_hit(unsigned m, unsigned c2) {
+  return (((m & 0x7FFF7FFFu) + c2) & 0x80008000u) != 0u;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
 }
 
-__device__ __noinline__ void slow8(const uint4 v, unsigned e0, unsigned tkey,
-                                      unsigned long long theta, SelState& s, int& ovf) {
-  const unsigned w[4] = {v.x, v.y, v.z, v.w};
+// Warp bitonic sort, descending, of NPER*32 keys held as a[r] at position r*32+lane.
+template <int NPER>
+__device__ __forceinline__ void warp_bitonic_desc(unsigned long long (&a)[NPER], int lane) {
+  constexpr int N = NPER * 32;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const unsigned b = (w[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
-    if ((b & 0x7FFFu) >= tkey) {
-      const unsigned long long key = make_key(b, e0 + i);
-      if (key >= theta) append_key(s, key, ovf);
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int rj = j >> 5;
+#pragma unroll
+        for (int r = 0; r < NPER; ++r) {
+          if ((r & rj) == 0) {
+            const bool desc = (((r * 32 + lane) & k) == 0);
+            const unsigned long long x = a[r], y = a[r | rj];
+            const unsigned long long hi = x > y ? x : y, lo = x > y ? y : x;
+            a[r] = desc ? hi : lo;
+            a[r | rj] = desc ? lo : hi;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < NPER; ++r) {
+          const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, a[r], j);
+          const bool desc = (((r * 32 + lane) & k) == 0);
+          const bool lower = (lane & j) == 0;
+          const unsigned long long hi = a[r] > o ? a[r] : o, lo = a[r] > o ? o : a[r];
+          a[r] = (desc == lower) ? hi : lo;
+        }
+      }
     }
   }
 }
 
+// Buffer full: keep the warp's kk largest keys, theta_w = the kk-th (rare path).
+__device__ __noinline__ unsigned long long warp_compact(unsigned long long* wb, int cnt, int kk, int lane) {
+  unsigned long long a[kWarpCap / 32];
+#pragma unroll
+  for (int r = 0; r < kWarpCap / 32; ++r) {
+    const int q = r * 32 + lane;
+    a[r] = q < cnt ? wb[q] : 0ull;
+  }
+  warp_bitonic_desc<kWarpCap / 32>(a, lane);
+#pragma unroll
+  for (int r = 0; r < kWarpCap / 32; ++r) wb[r * 32 + lane] = a[r];
+  __syncwarp();
+  return wb[kk - 1];
+}
+
+// Warp-uniform append of at most one key per lane.
+__device__ __forceinline__ void warp_append(bool p, unsigned long long key, unsigned long long* wb, int& cnt,
+                                            unsigned long long& theta, int kk, int lane) {
+  unsigned bal = __ballot_sync(0xFFFFFFFFu, p);
+  if (!bal) return;
+  if (cnt + __popc(bal) > kWarpCap) {
+    theta = warp_compact(wb, cnt, kk, lane);
+    cnt = kk;
+    p = p && key >= theta;
+    bal = __ballot_sync(0xFFFFFFFFu, p);
+  }
+  if (p) wb[cnt + __popc(bal & lanemask_lt())] = key;
+  cnt += __popc(bal);
+  __syncwarp();
+}
+
 // k-th largest of buf[0..n) by 8-bit radix select over the 56 significant bits.
-// All threads of the block must call; contains barriers.
+// All threads of the block must call; contains barriers.  Rare path.
 __device__ __noinline__ unsigned long long block_kth_largest(const unsigned long long* buf, int n, int k,
-                                                SelState& s) {
+                                                             SelState& s) {
   unsigned long long prefix = 0, mask = 0;
   int kr = k;
   for (int shift = 48; shift >= 0; shift -= 8) {
@@ -169,7 +244,7 @@ __device__ __noinline__ unsigned long long block_kth_largest(const unsigned long
         unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
         if (lane >= o) incl += y;
       }
-      unsigned excl = incl - sum;
+      const unsigned excl = incl - sum;
       if ((int)excl < kr && kr <= (int)incl) {
         unsigned acc = excl;
 #pragma unroll
@@ -191,136 +266,174 @@ __device__ __noinline__ unsigned long long block_kth_largest(const unsigned long
   return prefix;
 }
 
-// Buffer overflowed while processing tile [lo, hi): raise theta to the kk-th largest
-// buffered key (>= kk seen elements are >= it), drop this tile's entries (it is
-// re-processed against the new theta) and everything below theta.
-__device__ __noinline__ void handle_overflow(int lo, int hi, int kk, SelState& s) {
-  const unsigned long long th = block_kth_largest(s.buf, kCap, kk, s);
+// Final ranking when the warp buffers hold more than 256 candidates (ties,
+// degenerate chunks, theta = 0 restarts): radix-select the kk-th key over all
+// buffers, collect the kk keys >= it, sort them.  All threads call.
+__device__ __noinline__ void rank_many(int kk, int total, SelState& s) {
+  unsigned long long* all = &s.wbuf[0][0];
+  for (int e = threadIdx.x; e < kSelWarps * kWarpCap; e += kSelThreads)
+    if ((e % kWarpCap) >= s.wcnt[e / kWarpCap]) all[e] = 0ull;
   if (threadIdx.x == 0) s.n_out = 0;
   __syncthreads();
-  for (int e = threadIdx.x; e < kCap; e += kSelThreads) {
-    const unsigned long long v = s.buf[e];
-    const unsigned idx = key_idx(v);
-    if (v >= th && ((int)idx < lo || (int)idx >= hi)) s.out[atomicAdd(&s.n_out, 1)] = v;
-  }
+  const unsigned long long th = block_kth_largest(all, kSelWarps * kWarpCap, kk, s);
+  for (int e = threadIdx.x; e < kSelWarps * kWarpCap; e += kSelThreads)
+    if (all[e] >= th && all[e] != 0ull) s.out[atomicAdd(&s.n_out, 1)] = all[e];
   __syncthreads();
-  const int nk = s.n_out;
-  for (int e = threadIdx.x; e < nk; e += kSelThreads) s.buf[e] = s.out[e];
-  if (threadIdx.x == 0) {
-    s.n = nk;
-    s.theta = th;
-    s.spec = 0;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    unsigned long long a[TL_MAX_K / 32];
+#pragma unroll
+    for (int r = 0; r < TL_MAX_K / 32; ++r) a[r] = (r * 32 + lane < kk) ? s.out[r * 32 + lane] : 0ull;
+    __syncwarp();
+    warp_bitonic_desc<TL_MAX_K / 32>(a, lane);
+#pragma unroll
+    for (int r = 0; r < TL_MAX_K / 32; ++r) s.out[r * 32 + lane] = a[r];
   }
-  __syncthreads();
+  (void)total;
 }
 
-__device__ __noinline__ void rank_candidates(int kk, SelState& s);
-
 // Top-kk of one chunk (n contiguous bf16 at base) -> s.out[0..kk) in rank order.
-// Entry: s.theta / s.spec hold the threshold speculation for this chunk.
+// Entry: s.theta holds this chunk's speculative threshold.  Ends with a barrier.
 __device__ void select_chunk(const uint16_t* __restrict__ base, int n, int kk, SelState& s) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uintptr_t addr = reinterpret_cast<uintptr_t>(base);
   int a0 = (int)(((16u - (unsigned)(addr & 15u)) & 15u) >> 1);  // scalar head elements
   if (a0 > n) a0 = n;
   const int nvec = (n - a0) >> 3;
   const int tail0 = a0 + (nvec << 3);
-  const int ntiles = max(1, (nvec + kTileVec - 1) / kTileVec);
+  const int nit = (nvec + kTileVec - 1) / kTileVec;
   const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(base + a0);
+  unsigned long long* wb = s.wbuf[warp];
+  uint4* stg = s.stage[warp];
+  int* sidx = s.sidx[warp];
+  const uint16_t* stg16 = reinterpret_cast<const uint16_t*>(stg);
 
-  for (;;) {  // restarts only when a speculative theta proved too high
-    if (tid == 0) s.n = 0;
-    __syncthreads();
-    for (int t = 0; t < ntiles; ++t) {
-      const int lo = (t == 0) ? 0 : a0 + t * kTileElems;
-      const int hi = (t == ntiles - 1) ? n : a0 + (t + 1) * kTileElems;
-      for (;;) {
-        const unsigned long long theta = s.theta;
-        const unsigned tkey = (unsigned)(theta >> 40);
-        const unsigned tidx = key_idx(theta);
-        // elements of this tile tied with theta's magnitude lose on index once lo > tidx
-        const unsigned tk = tkey + ((unsigned)lo > tidx ? 1u : 0u);
-        const unsigned c2 = ((0x8000u - tk) & 0xFFFFu) * 0x10001u;
-        int ovf = 0;
-        uint4 v[kSelU];
+  int total;
+  for (;;) {
+    unsigned long long theta = s.theta;
+    const bool spec = theta != 0ull;
+    int cnt = 0;
+    if (warp == 0) {  // scalar head / tail elements
+      bool p = false;
+      unsigned long long key = 0;
+      if (lane < a0) { key = make_key(base[lane], lane); p = key >= theta; }
+      else if (lane >= 8 && lane - 8 < n - tail0) {
+        key = make_key(base[tail0 + lane - 8], tail0 + lane - 8);
+        p = key >= theta;
+      }
+      warp_append(p, key, wb, cnt, theta, kk, lane);
+    }
+    for (int it = 0; it < nit; ++it) {
+      const int gbase = it * kTileVec + warp * 32 + lane;
+      uint4 v[kSelU];
 #pragma unroll
-        for (int u = 0; u < kSelU; ++u) {
-          const int g = t * kTileVec + u * kSelThreads + tid;
-          if (g < nvec) v[u] = ld_stream(vb + g);
-        }
+      for (int u = 0; u < kSelU; ++u) {
+        const int g = gbase + u * kSelThreads;
+        v[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
+      }
+      const unsigned lo = (unsigned)(a0 + it * kTileElems);
+      const unsigned tkey = (unsigned)(theta >> 40);
+      // elements tied with theta's magnitude lose on index once lo > theta's index
+      const unsigned tk = tkey + (lo > key_idx(theta) ? 1u : 0u);
+      const unsigned c2 = ((0x8000u - tk) & 0xFFFFu) * 0x10001u;
+      unsigned mu[kSelU];
 #pragma unroll
-        for (int u = 0; u < kSelU; ++u) {
-          const int g = t * kTileVec + u * kSelThreads + tid;
-          if (g < nvec) {
-            const unsigned m = ((v[u].x & 0x7FFF7FFFu) + c2) | ((v[u].y & 0x7FFF7FFFu) + c2) |
-                               ((v[u].z & 0x7FFF7FFFu) + c2) | ((v[u].w & 0x7FFF7FFFu) + c2);
-            if (m & 0x80008000u) slow8(v[u], (unsigned)(a0 + 8 * g), tkey, theta, s, ovf);
-          }
+      for (int u = 0; u < kSelU; ++u) mu[u] = hmaxabs2(hmaxabs2(v[u].x, v[u].y), hmaxabs2(v[u].z, v[u].w));
+      unsigned m = mu[0];
+#pragma unroll
+      for (int u = 1; u < kSelU; ++u) m = hmaxabs2(m, mu[u]);
+      const bool hit = coarse_hit(m, c2);
+      if (!__any_sync(0xFFFFFFFFu, hit)) continue;
+      // stage this warp's flagged vectors, then test their elements lane-parallel
+      unsigned hm = 0;
+      if (hit) {
+#pragma unroll
+        for (int u = 0; u < kSelU; ++u) hm |= (coarse_hit(mu[u], c2) ? 1u : 0u) << u;
+      }
+      const int c = __popc(hm);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int pos = incl - c;
+      const int tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+#pragma unroll
+      for (int u = 0; u < kSelU; ++u) {
+        if ((hm >> u) & 1u) {
+          stg[pos] = v[u];
+          sidx[pos] = gbase + u * kSelThreads;
+          ++pos;
         }
-        if (t == 0 && tid < a0) {
-          const unsigned b = base[tid];
+      }
+      __syncwarp();
+      for (int e0 = 0; e0 < 8 * tot; e0 += 32) {
+        const int e = e0 + lane;
+        bool p = false;
+        unsigned long long key = 0;
+        if (e < 8 * tot) {
+          const unsigned b = stg16[e];
           if ((b & 0x7FFFu) >= tkey) {
-            const unsigned long long key = make_key(b, tid);
-            if (key >= theta) append_key(s, key, ovf);
+            key = make_key(b, (unsigned)(a0 + 8 * sidx[e >> 3] + (e & 7)));
+            p = key >= theta;
           }
         }
-        if (t == ntiles - 1 && tid < n - tail0) {
-          const unsigned b = base[tail0 + tid];
-          if ((b & 0x7FFFu) >= tkey) {
-            const unsigned long long key = make_key(b, tail0 + tid);
-            if (key >= theta) append_key(s, key, ovf);
-          }
-        }
-        if (!__syncthreads_or(ovf)) break;
-        handle_overflow(lo, hi, kk, s);
+        warp_append(p, key, wb, cnt, theta, kk, lane);
       }
     }
-    const int nf = s.n;
-    const int spec = s.spec;
+    if (lane == 0) s.wcnt[warp] = cnt;
     __syncthreads();
-    if (nf >= kk) break;
-    // speculative theta excluded part of the top-kk: redo the chunk exactly (theta = 0)
+    total = 0;
+#pragma unroll
+    for (int w = 0; w < kSelWarps; ++w) total += s.wcnt[w];
+    if (total >= kk) break;
+    // the speculative theta excluded part of the top-kk: redo the chunk exactly
     if (!spec) __trap();  // unreachable: theta = 0 admits every element
+    __syncthreads();
     if (tid == 0) {
-      s.theta = 0;
-      s.spec = 0;
-      s.delta = min(s.delta * 2, 0x4000);
+      s.theta = 0ull;
+      s.delta = min(s.delta + 4, 0x4000);
     }
     __syncthreads();
   }
 
-  rank_candidates(kk, s);
-}
-
-// Final ranking of the s.n candidates (keys are unique) into s.out[0..kk), then
-// the threshold speculation for this CTA's next chunk.
-__device__ __noinline__ void rank_candidates(int kk, SelState& s) {
-  const int tid = threadIdx.x;
-  const int nf = s.n;
-  unsigned long long th = 0;
-  if (nf > kRankDirect) th = block_kth_largest(s.buf, nf, kk, s);
-  for (int e = tid; e < nf; e += kSelThreads) {
-    const unsigned long long v = s.buf[e];
-    if (v >= th) {
-      int rank = 0;
-      for (int q = 0; q < nf; ++q) rank += (s.buf[q] > v) ? 1 : 0;
-      if (rank < kk) s.out[rank] = v;
+  if (total <= 256) {
+    if (warp == 0) {
+      unsigned long long a[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int q = r * 32 + lane;
+        int run = 0, w = 0, basew = 0;
+#pragma unroll
+        for (int t = 0; t < kSelWarps; ++t) {  // segment of q in the concatenated warp buffers
+          if (q >= run) { w = t; basew = run; }
+          run += s.wcnt[t];
+        }
+        a[r] = q < total ? s.wbuf[w][q - basew] : 0ull;
+      }
+      warp_bitonic_desc<8>(a, lane);
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r * 32 + lane < kk) s.out[r * 32 + lane] = a[r];
     }
+  } else {
+    rank_many(kk, total, s);
   }
   __syncthreads();
-  if (tid == 0) {
-    if (nf > kk + 256 && s.delta > 1) s.delta >>= 1;
+  if (tid == 0) {  // speculation for this CTA's next chunk
+    int d = s.delta;
+    if (total > kk + 128 && d > 1) --d;
+    else if (total < kk + 32) ++d;
+    s.delta = d;
     const unsigned kmag = (unsigned)(s.out[kk - 1] >> 40);
-    const unsigned d = (unsigned)s.delta;
-    s.theta = kmag > d ? ((unsigned long long)(kmag - d) << 40) : 0ull;
-    s.spec = s.theta != 0ull;
+    s.theta = kmag > (unsigned)d ? ((unsigned long long)(kmag - (unsigned)d) << 40) : 0ull;
   }
 }
 
 __device__ __forceinline__ void sel_init(SelState& s) {
   if (threadIdx.x == 0) {
     s.theta = 0;
-    s.spec = 0;
     s.delta = 8;
   }
   __syncthreads();
@@ -432,8 +545,64 @@ __global__ void inv_table_kernel(uint16_t* __restrict__ tables) {
     tables[(size_t)q * 65536u + a] = (a == 0 || a >= p) ? 0 : (uint16_t)m.pow(a, p - 2);
 }
 
-// One warp per chunk: modulus search, Newton divided differences over GF(p) with
-// table inverses, Newton -> monomial conversion, 258-byte serialisation.
+// Inverse source for the divided differences: the CTA's shared-memory table (first
+// prime, almost every chunk), a precomputed global table (primes 2..8), or Fermat.
+enum InvMode { kInvSmem = 0, kInvGlobal = 1, kInvFermat = 2 };
+
+template <int MODE>
+__device__ __forceinline__ uint32_t inv_of(const uint16_t* tab, uint32_t d, const ModP& m) {
+  if (MODE == kInvSmem) return tab[d];
+  if (MODE == kInvGlobal) return __ldg(tab + d);
+  return m.pow(d, m.p - 2);
+}
+
+// Interpolate the warp's kk points (x_i, y_i), i = lane + 32 r, over GF(p):
+// Newton divided differences, then Newton -> monomial.  Branch-free inner loops;
+// register blocks wholly below the active range are skipped warp-uniformly.
+template <int MODE>
+__device__ __forceinline__ void interpolate_warp(const uint32_t (&x)[4], uint32_t (&c)[4], uint32_t (&poly)[4],
+                                                 const uint32_t* xs, uint32_t* cs, int kk, const ModP& m,
+                                                 const uint16_t* tab, int lane) {
+  const int src = (lane + 31) & 31;
+  for (int jl = 1; jl < kk; ++jl) {
+    const int r0 = jl >> 5;
+    uint32_t t[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) t[r] = __shfl_sync(0xFFFFFFFFu, c[r], src);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (r < r0) continue;
+      const int i = lane + 32 * r;
+      const uint32_t prev = lane ? t[r] : (r ? t[r > 0 ? r - 1 : 0] : 0u);
+      const uint32_t d = m.sub(x[r], xs[max(i - jl, 0)]);
+      const uint32_t nv = m.mul(m.sub(c[r], prev), inv_of<MODE>(tab, d, m));
+      c[r] = i >= jl ? nv : c[r];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) cs[lane + 32 * r] = c[r];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 4; ++r) poly[r] = 0u;
+  if (lane == 0) poly[0] = cs[kk - 1];
+  for (int i = kk - 2; i >= 0; --i) {
+    const uint32_t xi = xs[i], ci = cs[i];
+    const int rmax = (kk - 1 - i) >> 5;
+    uint32_t t[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) t[r] = __shfl_sync(0xFFFFFFFFu, poly[r], src);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (r > rmax) continue;
+      const uint32_t prevk = lane ? t[r] : (r ? t[r > 0 ? r - 1 : 0] : (0u));
+      uint32_t nv = m.sub(prevk, m.mul(xi, poly[r]));
+      if (r == 0) nv = lane ? nv : m.add(nv, ci);
+      poly[r] = nv;
+    }
+  }
+}
+
+// One warp per chunk: modulus search, GF(p) interpolation, 258-byte serialisation.
 __global__ void __launch_bounds__(kCommitThreads, 1)
 commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits, int64_t n_chunks,
               int K, const uint16_t* __restrict__ inv_tables, uint8_t* __restrict__ proofs) {
@@ -477,11 +646,12 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
     if (maxidx >= kPMax) {
       for (pi = 0; pi < TL_N_PRIMES; ++pi) {
         p = kPrimesDesc[pi];
+        const ModP mp(p);
         uint32_t res[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int i = lane + 32 * r;
-          res[r] = (i < kk) ? raw[r] % p : 0x10000u + (uint32_t)i;
+          res[r] = (i < kk) ? mp.red(raw[r]) : 0x10000u + (uint32_t)i;
         }
         warp_sort128(res, lane);
         bool dup = false;
@@ -502,58 +672,19 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
       continue;
     }
     const ModP m(p);
-    const uint16_t* tab = (pi == 0) ? inv0 : (pi < kInvTables ? inv_tables + (size_t)pi * 65536u : nullptr);
-
-    uint32_t x[4], c[4];
+    uint32_t x[4], c[4], poly[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int i = lane + 32 * r;
-      x[r] = (i < kk) ? m.red(raw[r]) : 0;
-      c[r] = (i < kk) ? m.red(yb[r]) : 0;
+      x[r] = (i < kk) ? m.red(raw[r]) : 0u;
+      c[r] = (i < kk) ? m.red(yb[r]) : 0u;
       xs[i] = x[r];
     }
     __syncwarp();
-
-    // ---- Newton divided differences: c[i] <- (c[i] - c[i-1]) / (x[i] - x[i-jl])
-    for (int jl = 1; jl < kk; ++jl) {
-      const int r0 = jl >> 5;
-      uint32_t t[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) t[r] = __shfl_sync(0xFFFFFFFFu, c[r], (lane + 31) & 31);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        if (r < r0) continue;
-        const int i = lane + 32 * r;
-        if (i >= jl && i < kk) {
-          const uint32_t prev = lane ? t[r] : (r ? t[r ? r - 1 : 0] : 0u);
-          const uint32_t d = m.sub(x[r], xs[i - jl]);
-          const uint32_t inv = tab ? (uint32_t)tab[d] : m.pow(d, p - 2);
-          c[r] = m.mul(m.sub(c[r], prev), inv);
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) cs[lane + 32 * r] = c[r];
-    __syncwarp();
-
-    // ---- Newton -> monomial: poly <- poly * (X - x_i) + c_i, i = kk-2 .. 0
-    uint32_t poly[4] = {0u, 0u, 0u, 0u};
-    if (lane == 0) poly[0] = cs[kk - 1];
-    for (int i = kk - 2; i >= 0; --i) {
-      const uint32_t xi = xs[i], ci = cs[i];
-      const int deg = kk - 1 - i;
-      uint32_t t[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) t[r] = __shfl_sync(0xFFFFFFFFu, poly[r], (lane + 31) & 31);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        if (32 * r > deg) continue;
-        const uint32_t prevk = lane ? t[r] : (r ? t[r ? r - 1 : 0] : 0u);
-        uint32_t nv = m.sub(prevk, m.mul(xi, poly[r]));
-        if (lane == 0 && r == 0) nv = m.add(nv, ci);
-        poly[r] = nv;
-      }
-    }
+    if (pi == 0) interpolate_warp<kInvSmem>(x, c, poly, xs, cs, kk, m, inv0, lane);
+    else if (pi < kInvTables)
+      interpolate_warp<kInvGlobal>(x, c, poly, xs, cs, kk, m, inv_tables + (size_t)pi * 65536u, lane);
+    else interpolate_warp<kInvFermat>(x, c, poly, xs, cs, kk, m, nullptr, lane);
 
     // ---- serialise: p, c_0..c_{K-1}, u16 big-endian
     uint16_t* pw = reinterpret_cast<uint16_t*>(pr);
