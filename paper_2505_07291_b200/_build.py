@@ -39,21 +39,22 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    lib = out or LIB
+    if not force and out is None and not needs_build():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *NVCC_FLAGS, "-o", tmp, SRC, "-lcudart"]
+    tmp = lib + ".tmp"
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", tmp, SRC, "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr}")
     if verbose:
         sys.stderr.write(res.stderr)
-    with open(os.path.join(OUT_DIR, "ptxas.log"), "w") as f:
+    with open(lib + ".ptxas.log" if out else os.path.join(OUT_DIR, "ptxas.log"), "w") as f:
         f.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -61,7 +61,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        path = _build.LIB
+        path = os.environ.get("TOPLOC_B200_LIB", _build.LIB)  # experiments: alternative builds
         if not os.path.exists(path):
             if not build_if_missing:
                 raise RuntimeError(f"CUDA extension missing: {path} (run __graft_entry__.build())")

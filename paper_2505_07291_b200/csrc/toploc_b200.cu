@@ -28,7 +28,13 @@ namespace {
 // ----------------------------------------------------------------------------- constants
 constexpr int kSelThreads = 256;              // select CTA
 constexpr int kSelU = 4;                      // 16-B vectors per thread per tile
-constexpr int kSelMinBlocks = 4;              // resident select CTAs per SM (<= 64 regs)
+#ifndef TL_SEL_MIN_BLOCKS
+#define TL_SEL_MIN_BLOCKS 4
+#endif
+#ifndef TL_DBUF
+#define TL_DBUF 1
+#endif
+constexpr int kSelMinBlocks = TL_SEL_MIN_BLOCKS;  // resident select CTAs per SM (3 -> <= 80 regs)
 constexpr int kTileVec = kSelThreads * kSelU; // 1024 vectors = 8192 bf16 per tile
 constexpr int kTileElems = kTileVec * 8;
 constexpr int kSelWarps = kSelThreads / 32;
@@ -59,19 +65,24 @@ __device__ __forceinline__ unsigned key_idx(unsigned long long s) {
   return kIdxMask - (unsigned)((s >> 16) & kIdxMask);
 }
 
+// Arithmetic mod p (2 <= p < 2^16) on u32.  Reductions use the unsigned-min trick:
+// for r in [0, 2p), min(r, r - p) (mod 2^32) is r mod p -- one VIADDMNMX.
 struct ModP {
-  uint32_t p, mu;  // mu = floor(2^32 / p), p >= 2
-  __device__ __forceinline__ explicit ModP(uint32_t p_) : p(p_), mu((uint32_t)(0x100000000ull / p_)) {}
-  __device__ __forceinline__ uint32_t red(uint32_t t) const {  // t < 2^32 -> t mod p
-    uint32_t q = __umulhi(t, mu);
-    uint32_t r = t - q * p;
-    return r >= p ? r - p : r;
+  uint32_t p, np, mu;  // np = -p mod 2^32, mu = floor(2^32 / p)
+  __device__ __forceinline__ explicit ModP(uint32_t p_)
+      : p(p_), np(0u - p_), mu((uint32_t)(0x100000000ull / p_)) {}
+  __device__ __forceinline__ uint32_t red(uint32_t t) const {  // t < 2^32 -> t mod p (Barrett)
+    const uint32_t r = t + __umulhi(t, mu) * np;                 // t - q p, in [0, 2p)
+    return min(r, r + np);
   }
   __device__ __forceinline__ uint32_t mul(uint32_t a, uint32_t b) const { return red(a * b); }
-  __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) const { return a >= b ? a - b : a + p - b; }
+  __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) const {
+    const uint32_t t = a - b;  // a, b < p
+    return min(t, t + p);
+  }
   __device__ __forceinline__ uint32_t add(uint32_t a, uint32_t b) const {
-    uint32_t s = a + b;
-    return s >= p ? s - p : s;
+    const uint32_t s = a + b;
+    return min(s, s + np);
   }
   __device__ uint32_t pow(uint32_t a, uint32_t e) const {
     uint32_t r = 1;
@@ -124,7 +135,7 @@ __device__ __forceinline__ ChunkRef locate_chunk(const int64_t* __restrict__ pre
 struct SelState {
   unsigned long long wbuf[kSelWarps][kWarpCap];  // per-warp candidate keys
   uint4 stage[kSelWarps][kStageVec];             // per-warp flagged vectors
-  int sidx[kSelWarps][kStageVec];                // their vector index
+  int sidx[kSelWarps][kStageVec];                // their vector index (scan staging)
   unsigned long long out[TL_MAX_K];              // selected keys, rank order
   unsigned long long theta;                      // chunk-start threshold (speculation)
   int wcnt[kSelWarps];
@@ -137,6 +148,7 @@ struct SelState {
   unsigned p;
   unsigned mism, nmatch, msum;
   unsigned mhist[128];
+  uint32_t hpart[TL_MAX_K];
   uint16_t coef[TL_MAX_K];
 };
 
@@ -323,13 +335,29 @@ __device__ void select_chunk(const uint16_t* __restrict__ base, int n, int kk, S
       }
       warp_append(p, key, wb, cnt, theta, kk, lane);
     }
+#if TL_DBUF
+    // register double buffer: the next iteration's 16-B loads are in flight while
+    // this one is filtered
+    uint4 vn[kSelU];
+#pragma unroll
+    for (int u = 0; u < kSelU; ++u) {
+      const int g = warp * 32 + lane + u * kSelThreads;
+      vn[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#endif
     for (int it = 0; it < nit; ++it) {
       const int gbase = it * kTileVec + warp * 32 + lane;
       uint4 v[kSelU];
 #pragma unroll
       for (int u = 0; u < kSelU; ++u) {
+#if TL_DBUF
+        v[u] = vn[u];
+        const int g = gbase + kTileVec + u * kSelThreads;
+        vn[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
+#else
         const int g = gbase + u * kSelThreads;
         v[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
+#endif
       }
       const unsigned lo = (unsigned)(a0 + it * kTileElems);
       const unsigned tkey = (unsigned)(theta >> 40);
@@ -344,11 +372,13 @@ __device__ void select_chunk(const uint16_t* __restrict__ base, int n, int kk, S
       for (int u = 1; u < kSelU; ++u) m = hmaxabs2(m, mu[u]);
       const bool hit = coarse_hit(m, c2);
       if (!__any_sync(0xFFFFFFFFu, hit)) continue;
-      // stage this warp's flagged vectors, then test their elements lane-parallel
+      // compact this warp's flagged vectors into its staging area (warp scan), then
+      // test their elements lane-parallel
       unsigned hm = 0;
       if (hit) {
 #pragma unroll
-        for (int u = 0; u < kSelU; ++u) hm |= (coarse_hit(mu[u], c2) ? 1u : 0u) << u;
+        for (int u = 0; u < kSelU; ++u)
+          hm |= ((gbase + u * kSelThreads < nvec && coarse_hit(mu[u], c2)) ? 1u : 0u) << u;
       }
       const int c = __popc(hm);
       int incl = c;
@@ -556,50 +586,70 @@ __device__ __forceinline__ uint32_t inv_of(const uint16_t* tab, uint32_t d, cons
   return m.pow(d, m.p - 2);
 }
 
+// Newton divided differences, levels jl in [j0, j1) with j1 <= 32 (R0 + 1): the
+// register blocks r < R0 are complete (i < jl) and skipped at compile time; in
+// block R0 lanes with i < jl keep their value.  c[i] <- (c[i] - c[i-1]) / (x[i] - x[i-jl]).
+template <int MODE, int R0>
+__device__ __forceinline__ void ndd_levels(int j0, int j1, const uint32_t (&x)[4], uint32_t (&c)[4],
+                                           const uint32_t* xs, const ModP& m, const uint16_t* tab, int lane) {
+  const int src = (lane + 31) & 31;
+  for (int jl = j0; jl < j1; ++jl) {
+    uint32_t t[4];
+#pragma unroll
+    for (int r = (R0 > 0 ? R0 - 1 : 0); r < 4; ++r) t[r] = __shfl_sync(0xFFFFFFFFu, c[r], src);
+#pragma unroll
+    for (int r = R0; r < 4; ++r) {
+      const int i = lane + 32 * r;
+      const uint32_t prev = lane ? t[r] : (r ? t[r > 0 ? r - 1 : 0] : 0u);
+      const uint32_t xj = xs[r == R0 ? max(i - jl, 0) : i - jl];
+      const uint32_t nv = m.mul(m.sub(c[r], prev), inv_of<MODE>(tab, m.sub(x[r], xj), m));
+      if (r > R0 || i >= jl) c[r] = nv;
+    }
+  }
+}
+
+// Newton -> monomial steps i in [i_lo, i_hi] (descending): poly <- poly * (X - x_i) + c_i.
+// The polynomial has degree kk-1-i <= 32 (RM + 1) - 1, so blocks r > RM stay zero.
+template <int RM>
+__device__ __forceinline__ void conv_steps(int i_hi, int i_lo, uint32_t (&poly)[4], const uint32_t* xs,
+                                           const uint32_t* cs, const ModP& m, int lane) {
+  const int src = (lane + 31) & 31;
+  for (int i = i_hi; i >= i_lo; --i) {
+    const uint32_t xi = xs[i], ci = cs[i];
+    uint32_t t[4];
+#pragma unroll
+    for (int r = 0; r <= RM; ++r) t[r] = __shfl_sync(0xFFFFFFFFu, poly[r], src);
+#pragma unroll
+    for (int r = 0; r <= RM; ++r) {
+      const uint32_t prevk = lane ? t[r] : (r ? t[r > 0 ? r - 1 : 0] : (0u));
+      uint32_t nv = m.sub(prevk, m.mul(xi, poly[r]));
+      if (r == 0 && lane == 0) nv = m.add(nv, ci);
+      poly[r] = nv;
+    }
+  }
+}
+
 // Interpolate the warp's kk points (x_i, y_i), i = lane + 32 r, over GF(p):
-// Newton divided differences, then Newton -> monomial.  Branch-free inner loops;
-// register blocks wholly below the active range are skipped warp-uniformly.
+// Newton divided differences, then Newton -> monomial.
 template <int MODE>
 __device__ __forceinline__ void interpolate_warp(const uint32_t (&x)[4], uint32_t (&c)[4], uint32_t (&poly)[4],
                                                  const uint32_t* xs, uint32_t* cs, int kk, const ModP& m,
                                                  const uint16_t* tab, int lane) {
-  const int src = (lane + 31) & 31;
-  for (int jl = 1; jl < kk; ++jl) {
-    const int r0 = jl >> 5;
-    uint32_t t[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) t[r] = __shfl_sync(0xFFFFFFFFu, c[r], src);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (r < r0) continue;
-      const int i = lane + 32 * r;
-      const uint32_t prev = lane ? t[r] : (r ? t[r > 0 ? r - 1 : 0] : 0u);
-      const uint32_t d = m.sub(x[r], xs[max(i - jl, 0)]);
-      const uint32_t nv = m.mul(m.sub(c[r], prev), inv_of<MODE>(tab, d, m));
-      c[r] = i >= jl ? nv : c[r];
-    }
-  }
+  ndd_levels<MODE, 0>(1, min(kk, 32), x, c, xs, m, tab, lane);
+  ndd_levels<MODE, 1>(32, min(kk, 64), x, c, xs, m, tab, lane);
+  ndd_levels<MODE, 2>(64, min(kk, 96), x, c, xs, m, tab, lane);
+  ndd_levels<MODE, 3>(96, kk, x, c, xs, m, tab, lane);
 #pragma unroll
   for (int r = 0; r < 4; ++r) cs[lane + 32 * r] = c[r];
   __syncwarp();
 #pragma unroll
   for (int r = 0; r < 4; ++r) poly[r] = 0u;
   if (lane == 0) poly[0] = cs[kk - 1];
-  for (int i = kk - 2; i >= 0; --i) {
-    const uint32_t xi = xs[i], ci = cs[i];
-    const int rmax = (kk - 1 - i) >> 5;
-    uint32_t t[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) t[r] = __shfl_sync(0xFFFFFFFFu, poly[r], src);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (r > rmax) continue;
-      const uint32_t prevk = lane ? t[r] : (r ? t[r > 0 ? r - 1 : 0] : (0u));
-      uint32_t nv = m.sub(prevk, m.mul(xi, poly[r]));
-      if (r == 0) nv = lane ? nv : m.add(nv, ci);
-      poly[r] = nv;
-    }
-  }
+  // step i yields degree kk-1-i: blocks r <= (kk-1-i) >> 5 are live
+  conv_steps<0>(kk - 2, max(kk - 32, 0), poly, xs, cs, m, lane);
+  conv_steps<1>(kk - 33, max(kk - 64, 0), poly, xs, cs, m, lane);
+  conv_steps<2>(kk - 65, max(kk - 96, 0), poly, xs, cs, m, lane);
+  conv_steps<3>(kk - 97, 0, poly, xs, cs, m, lane);
 }
 
 // One warp per chunk: modulus search, GF(p) interpolation, 258-byte serialisation.
@@ -727,18 +777,28 @@ verify_kernel(const uint16_t* __restrict__ hidden, const int64_t* __restrict__ r
     __syncthreads();
     const unsigned p = s.p;
     const bool bad = p < 2;
-    if (!bad && tid < kk) {
+    // Horner split over the two halves of the block: thread t < 128 evaluates
+    // c_0..c_{h-1} at point t, thread t + 128 evaluates c_h..c_{K-1} and scales by x^h
+    const int pt = tid & 127, half = tid >> 7, h = (K + 1) >> 1;
+    uint32_t acc = 0, x = 0;
+    if (!bad && pt < kk) {
       const ModP m(p);
-      const unsigned long long v = s.out[tid];
-      const uint32_t x = m.red(key_idx(v));
+      x = m.red(key_idx(s.out[pt]));
+      const int k_lo = half ? h : 0, k_hi = half ? K : h;
+      for (int k = k_hi - 1; k >= k_lo; --k) acc = m.red(acc * x + (uint32_t)s.coef[k]);
+      if (half) s.hpart[pt] = m.mul(acc, m.pow(x, (uint32_t)h));
+    }
+    __syncthreads();
+    if (!bad && half == 0 && pt < kk) {
+      const ModP m(p);
+      const unsigned long long v = s.out[pt];
+      const uint32_t claimed = m.add(acc, s.hpart[pt]);
       const uint32_t obs = m.red((uint32_t)(v & 0xFFFFu));
-      uint32_t acc = 0;
-      for (int k = K - 1; k >= 0; --k) acc = m.red(acc * x + (uint32_t)s.coef[k]);
-      const uint32_t ce = (acc >> 7) & 0xFFu, oe = (obs >> 7) & 0xFFu;
+      const uint32_t ce = (claimed >> 7) & 0xFFu, oe = (obs >> 7) & 0xFFu;
       if (ce != oe) {
         atomicAdd(&s.mism, 1u);
       } else {
-        const int d = abs((int)(acc & 0x7Fu) - (int)(obs & 0x7Fu));
+        const int d = abs((int)(claimed & 0x7Fu) - (int)(obs & 0x7Fu));
         atomicAdd(&s.mhist[d], 1u);
         atomicAdd(&s.msum, (unsigned)d);
         atomicAdd(&s.nmatch, 1u);
