@@ -26,20 +26,26 @@
 namespace {
 
 // ----------------------------------------------------------------------------- constants
-constexpr int kSelThreads = 256;              // select CTA
+#ifndef TL_RING
+#define TL_RING 0  // TMA ring select (1) or direct register-double-buffered loads (0)
+#endif
+constexpr int kSelThreads = 256;              // select CTA consumer threads (8 warps)
 constexpr int kSelU = 4;                      // 16-B vectors per thread per tile
 #ifndef TL_SEL_MIN_BLOCKS
-#define TL_SEL_MIN_BLOCKS 4
+#define TL_SEL_MIN_BLOCKS (TL_RING ? 2 : 4)
 #endif
-#ifndef TL_DBUF
-#define TL_DBUF 1
-#endif
-constexpr int kSelMinBlocks = TL_SEL_MIN_BLOCKS;  // resident select CTAs per SM (3 -> <= 80 regs)
+constexpr int kSelMinBlocks = TL_SEL_MIN_BLOCKS;  // resident select CTAs per SM
 constexpr int kTileVec = kSelThreads * kSelU; // 1024 vectors = 8192 bf16 per tile
 constexpr int kTileElems = kTileVec * 8;
 constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kWarpCap = 256;                 // per-warp candidate buffer (2 KiB)
-constexpr int kStageVec = 32 * kSelU;         // per-warp staging: every vector of one iteration
+static_assert(kWarpCap >= TL_MAX_K + 32, "a compaction must leave room for one full ballot");
+constexpr int kStageVec = 32 * kSelU;         // per-warp flagged-vector list (every vector of a batch)
+#ifndef TL_RING_STAGES
+#define TL_RING_STAGES 5
+#endif
+constexpr int kRingStages = TL_RING_STAGES;   // 16 KiB TMA stages per CTA
+constexpr int kRingStageBytes = kTileVec * 16;
 constexpr unsigned kIdxMask = 0xFFFFFFu;      // flat index field (24 bits)
 constexpr int kInvTables = 8;                 // precomputed inverse tables (first 8 primes)
 constexpr int kCommitWarps = 16;
@@ -120,22 +126,32 @@ __device__ __forceinline__ ChunkRef locate_chunk(const int64_t* __restrict__ pre
 
 // ----------------------------------------------------------------------------- streaming select
 //
-// One CTA owns one chunk at a time (persistent over chunks).  Each warp streams an
-// interleaved share of the chunk's 16-byte vectors and keeps its own candidate
-// buffer and threshold theta_w with the invariant
+// One CTA owns one chunk at a time (persistent over its chunks j = blockIdx.x,
+// + gridDim.x, ...).  TL_RING=1 (default): a producer warp streams the CTA's chunks
+// through a ring of kRingStages x 16 KiB shared-memory stages with TMA bulk copies
+// (cp.async.bulk + mbarrier complete_tx), running ahead across chunk boundaries so
+// ~190 KiB per SM stay in flight -- the depth a pure read needs to approach the
+// ~7.3 TB/s read ceiling measured on this part (tools/lab/bwprobe.py).  Eight
+// consumer warps filter each stage (1024 vectors, 128 per warp).  TL_RING=0: the
+// consumers load straight from HBM with a register double buffer.
+//
+// Each consumer warp keeps its own candidate buffer and threshold theta_w with
+// the invariant
 //     every element this warp has seen with key >= theta_w is in its buffer,
 // and, once theta_w was raised by a compaction, >= kk seen elements are >= theta_w.
 // The union of the warp buffers therefore contains the chunk's top-kk (an element
-// below its warp's theta_w is beaten by kk others).  No block barrier is needed
-// while streaming; the chunk ends with one barrier and a warp bitonic sort.
+// below its warp's theta_w is beaten by kk others).  No barrier while streaming;
+// the chunk ends with one consumer barrier and a warp bitonic sort.
 //
-// The chunk starts from a speculative theta (the previous chunk's kk-th magnitude
+// A chunk starts from a speculative theta (the previous chunk's kk-th magnitude
 // minus an adaptive margin).  If the union ends with < kk entries the speculation
-// was too high and the chunk is redone from theta = 0 (L2-resident re-read).
+// was too high and the chunk is re-scanned from HBM/L2 with theta = 0.
 struct SelState {
   unsigned long long wbuf[kSelWarps][kWarpCap];  // per-warp candidate keys
-  uint4 stage[kSelWarps][kStageVec];             // per-warp flagged vectors
-  int sidx[kSelWarps][kStageVec];                // their vector index (scan staging)
+  int sidx[kSelWarps][kStageVec];                // per-warp flagged vector ids
+#if !TL_RING
+  uint4 stage[kSelWarps][kStageVec];             // flagged vectors copied out of registers
+#endif
   unsigned long long out[TL_MAX_K];              // selected keys, rank order
   unsigned long long theta;                      // chunk-start threshold (speculation)
   int wcnt[kSelWarps];
@@ -151,6 +167,17 @@ struct SelState {
   uint32_t hpart[TL_MAX_K];
   uint16_t coef[TL_MAX_K];
 };
+constexpr size_t kSelStateBytes = (sizeof(SelState) + 127) & ~(size_t)127;
+#if TL_RING
+constexpr int kSelBlockThreads = kSelThreads + 32;  // + producer warp
+constexpr size_t kSelSmem = kSelStateBytes + (size_t)kRingStages * kRingStageBytes + 2 * kRingStages * 8;
+#else
+constexpr int kSelBlockThreads = kSelThreads;
+constexpr size_t kSelSmem = kSelStateBytes;
+#endif
+
+// Barrier over the consumer threads only (the producer warp never joins).
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(kSelThreads) : "memory"); }
 
 __device__ __forceinline__ unsigned hmaxabs2(unsigned a, unsigned b) {
   unsigned d;  // per bf16 half: max(|a|, |b|) (sign = xor, masked off by the caller); NaN wins
@@ -164,6 +191,63 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned r;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
   return r;
+}
+
+// ---- TMA bulk copy + mbarrier primitives
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+
+// ---- chunk geometry
+struct ChunkGeo {
+  const uint16_t* base;  // first element
+  int n;                 // elements
+  int a0;                // scalar head elements before the first 16-B boundary
+  int nvec;              // 16-B vectors after the head
+  int nst;               // 1024-vector stages
+};
+struct SelArgs {
+  const uint16_t* hidden;
+  const int64_t* row_off;
+  const int64_t* prefix;
+  int n_roll, H, C, K;
+  int64_t n_chunks;  // min(caller's n_chunks, prefix[n_roll])
+};
+__device__ __forceinline__ ChunkGeo chunk_geo(const SelArgs& a, int64_t j) {
+  const ChunkRef cr = locate_chunk(a.prefix, a.row_off, a.n_roll, j, a.C);
+  ChunkGeo g;
+  g.base = a.hidden + cr.row_start * (int64_t)a.H;
+  g.n = cr.rows * a.H;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(g.base);
+  g.a0 = min(g.n, (int)(((16u - (unsigned)(addr & 15u)) & 15u) >> 1));
+  g.nvec = (g.n - g.a0) >> 3;
+  g.nst = (g.nvec + kTileVec - 1) / kTileVec;
+  return g;
 }
 
 // Warp bitonic sort, descending, of NPER*32 keys held as a[r] at position r*32+lane.
@@ -200,7 +284,7 @@ __device__ __forceinline__ void warp_bitonic_desc(unsigned long long (&a)[NPER],
   }
 }
 
-// Buffer full: keep the warp's kk largest keys, theta_w = the kk-th (rare path).
+// Buffer full: keep the warp's kk largest keys; returns theta_w = the kk-th (rare path).
 __device__ __noinline__ unsigned long long warp_compact(unsigned long long* wb, int cnt, int kk, int lane) {
   unsigned long long a[kWarpCap / 32];
 #pragma unroll
@@ -232,19 +316,19 @@ __device__ __forceinline__ void warp_append(bool p, unsigned long long key, unsi
 }
 
 // k-th largest of buf[0..n) by 8-bit radix select over the 56 significant bits.
-// All threads of the block must call; contains barriers.  Rare path.
+// All consumer threads call; contains barriers.  Rare path.
 __device__ __noinline__ unsigned long long block_kth_largest(const unsigned long long* buf, int n, int k,
                                                              SelState& s) {
   unsigned long long prefix = 0, mask = 0;
   int kr = k;
   for (int shift = 48; shift >= 0; shift -= 8) {
-    s.hist[threadIdx.x] = 0;  // blockDim == 256 == bins
-    __syncthreads();
+    if (threadIdx.x < 256) s.hist[threadIdx.x] = 0;
+    csync();
     for (int e = threadIdx.x; e < n; e += kSelThreads) {
       const unsigned long long v = buf[e];
       if ((v & mask) == prefix) atomicAdd(&s.hist[(unsigned)(v >> shift) & 255u], 1u);
     }
-    __syncthreads();
+    csync();
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x;
       unsigned c[8], sum = 0;
@@ -269,28 +353,28 @@ __device__ __noinline__ unsigned long long block_kth_largest(const unsigned long
         }
       }
     }
-    __syncthreads();
+    csync();
     prefix |= (unsigned long long)s.digit << shift;
     mask |= 0xFFull << shift;
     kr = s.kr;
-    __syncthreads();
+    csync();
   }
   return prefix;
 }
 
 // Final ranking when the warp buffers hold more than 256 candidates (ties,
 // degenerate chunks, theta = 0 restarts): radix-select the kk-th key over all
-// buffers, collect the kk keys >= it, sort them.  All threads call.
-__device__ __noinline__ void rank_many(int kk, int total, SelState& s) {
+// buffers, collect the kk keys >= it, sort them.  All consumer threads call.
+__device__ __noinline__ void rank_many(int kk, SelState& s) {
   unsigned long long* all = &s.wbuf[0][0];
   for (int e = threadIdx.x; e < kSelWarps * kWarpCap; e += kSelThreads)
     if ((e % kWarpCap) >= s.wcnt[e / kWarpCap]) all[e] = 0ull;
   if (threadIdx.x == 0) s.n_out = 0;
-  __syncthreads();
+  csync();
   const unsigned long long th = block_kth_largest(all, kSelWarps * kWarpCap, kk, s);
   for (int e = threadIdx.x; e < kSelWarps * kWarpCap; e += kSelThreads)
     if (all[e] >= th && all[e] != 0ull) s.out[atomicAdd(&s.n_out, 1)] = all[e];
-  __syncthreads();
+  csync();
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     unsigned long long a[TL_MAX_K / 32];
@@ -301,131 +385,236 @@ __device__ __noinline__ void rank_many(int kk, int total, SelState& s) {
 #pragma unroll
     for (int r = 0; r < TL_MAX_K / 32; ++r) s.out[r * 32 + lane] = a[r];
   }
-  (void)total;
 }
 
-// Top-kk of one chunk (n contiguous bf16 at base) -> s.out[0..kk) in rank order.
-// Entry: s.theta holds this chunk's speculative threshold.  Ends with a barrier.
-__device__ void select_chunk(const uint16_t* __restrict__ base, int n, int kk, SelState& s) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uintptr_t addr = reinterpret_cast<uintptr_t>(base);
-  int a0 = (int)(((16u - (unsigned)(addr & 15u)) & 15u) >> 1);  // scalar head elements
-  if (a0 > n) a0 = n;
-  const int nvec = (n - a0) >> 3;
-  const int tail0 = a0 + (nvec << 3);
-  const int nit = (nvec + kTileVec - 1) / kTileVec;
-  const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(base + a0);
-  unsigned long long* wb = s.wbuf[warp];
-  uint4* stg = s.stage[warp];
-  int* sidx = s.sidx[warp];
-  const uint16_t* stg16 = reinterpret_cast<const uint16_t*>(stg);
+// Per-warp streaming state (all members warp-uniform except the pointers' targets).
+struct WarpScan {
+  unsigned long long theta;
+  int cnt;
+  unsigned long long* wb;
+  int* sidx;    // flagged vector ids of the current batch
+  uint4* stg;   // TL_RING=0: flagged vectors copied out of registers
+};
 
-  int total;
-  for (;;) {
-    unsigned long long theta = s.theta;
-    const bool spec = theta != 0ull;
-    int cnt = 0;
-    if (warp == 0) {  // scalar head / tail elements
-      bool p = false;
-      unsigned long long key = 0;
-      if (lane < a0) { key = make_key(base[lane], lane); p = key >= theta; }
-      else if (lane >= 8 && lane - 8 < n - tail0) {
-        key = make_key(base[tail0 + lane - 8], tail0 + lane - 8);
-        p = key >= theta;
+__device__ __forceinline__ unsigned coarse_c2(unsigned long long theta, unsigned lo) {
+  const unsigned tkey = (unsigned)(theta >> 40);
+  // elements tied with theta's magnitude lose on index once lo > theta's index
+  const unsigned tk = tkey + (lo > key_idx(theta) ? 1u : 0u);
+  return ((0x8000u - tk) & 0xFFFFu) * 0x10001u;
+}
+
+// Test the elements of `nflag` flagged vectors lane-parallel and append survivors.
+// Element e of the batch is vector sidx[e >> 3], bf16 (e & 7); its bits are read
+// through `elem(e)`.
+template <typename Elem>
+__device__ __forceinline__ void test_flagged(int nflag, int a0, WarpScan& w, int kk, int lane, Elem elem) {
+  const unsigned tkey = (unsigned)(w.theta >> 40);
+  for (int e0 = 0; e0 < 8 * nflag; e0 += 32) {
+    const int e = e0 + lane;
+    bool p = false;
+    unsigned long long key = 0;
+    if (e < 8 * nflag) {
+      const unsigned b = elem(e);
+      if ((b & 0x7FFFu) >= tkey) {
+        key = make_key(b, (unsigned)(a0 + 8 * w.sidx[e >> 3] + (e & 7)));
+        p = key >= w.theta;
       }
-      warp_append(p, key, wb, cnt, theta, kk, lane);
     }
-#if TL_DBUF
-    // register double buffer: the next iteration's 16-B loads are in flight while
-    // this one is filtered
-    uint4 vn[kSelU];
+    warp_append(p, key, w.wb, w.cnt, w.theta, kk, lane);
+  }
+}
+
+// Chunk pass straight from HBM/L2 with a register double buffer.  Vector g of tile
+// t: t*1024 + u*256 + warp*32 + lane.  Flagged vectors are copied to w.stg
+// (STAGE) or their elements re-read from global memory (L2-hot; the TL_RING
+// restart path, which has no staging buffer).
+template <bool STAGE>
+__device__ __forceinline__ void pass_ldg(const ChunkGeo& cg, WarpScan& w, int kk, int warp, int lane) {
+  const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(cg.base + cg.a0);
+  const int nvec = cg.nvec, a0 = cg.a0;
+  uint4 vn[kSelU];
+#pragma unroll
+  for (int u = 0; u < kSelU; ++u) {
+    const int g = warp * 32 + lane + u * kSelThreads;
+    vn[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
+  }
+  for (int it = 0; it < cg.nst; ++it) {
+    const int gbase = it * kTileVec + warp * 32 + lane;
+    uint4 v[kSelU];
 #pragma unroll
     for (int u = 0; u < kSelU; ++u) {
-      const int g = warp * 32 + lane + u * kSelThreads;
+      v[u] = vn[u];
+      const int g = gbase + kTileVec + u * kSelThreads;
       vn[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
     }
-#endif
-    for (int it = 0; it < nit; ++it) {
-      const int gbase = it * kTileVec + warp * 32 + lane;
-      uint4 v[kSelU];
+    const unsigned c2 = coarse_c2(w.theta, (unsigned)(a0 + it * kTileElems));
+    unsigned mu[kSelU];
 #pragma unroll
-      for (int u = 0; u < kSelU; ++u) {
-#if TL_DBUF
-        v[u] = vn[u];
-        const int g = gbase + kTileVec + u * kSelThreads;
-        vn[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
-#else
-        const int g = gbase + u * kSelThreads;
-        v[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
-#endif
-      }
-      const unsigned lo = (unsigned)(a0 + it * kTileElems);
-      const unsigned tkey = (unsigned)(theta >> 40);
-      // elements tied with theta's magnitude lose on index once lo > theta's index
-      const unsigned tk = tkey + (lo > key_idx(theta) ? 1u : 0u);
-      const unsigned c2 = ((0x8000u - tk) & 0xFFFFu) * 0x10001u;
-      unsigned mu[kSelU];
+    for (int u = 0; u < kSelU; ++u) mu[u] = hmaxabs2(hmaxabs2(v[u].x, v[u].y), hmaxabs2(v[u].z, v[u].w));
+    unsigned m = mu[0];
 #pragma unroll
-      for (int u = 0; u < kSelU; ++u) mu[u] = hmaxabs2(hmaxabs2(v[u].x, v[u].y), hmaxabs2(v[u].z, v[u].w));
-      unsigned m = mu[0];
+    for (int u = 1; u < kSelU; ++u) m = hmaxabs2(m, mu[u]);
+    const bool hit = coarse_hit(m, c2);
+    if (!__any_sync(0xFFFFFFFFu, hit)) continue;
+    unsigned hm = 0;
+    if (hit) {
 #pragma unroll
-      for (int u = 1; u < kSelU; ++u) m = hmaxabs2(m, mu[u]);
-      const bool hit = coarse_hit(m, c2);
-      if (!__any_sync(0xFFFFFFFFu, hit)) continue;
-      // compact this warp's flagged vectors into its staging area (warp scan), then
-      // test their elements lane-parallel
-      unsigned hm = 0;
-      if (hit) {
+      for (int u = 0; u < kSelU; ++u)
+        hm |= ((gbase + u * kSelThreads < nvec && coarse_hit(mu[u], c2)) ? 1u : 0u) << u;
+    }
+    const int c = __popc(hm);
+    int incl = c;
 #pragma unroll
-        for (int u = 0; u < kSelU; ++u)
-          hm |= ((gbase + u * kSelThreads < nvec && coarse_hit(mu[u], c2)) ? 1u : 0u) << u;
-      }
-      const int c = __popc(hm);
-      int incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int pos = incl - c;
+    const int tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      int pos = incl - c;
-      const int tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
-#pragma unroll
-      for (int u = 0; u < kSelU; ++u) {
-        if ((hm >> u) & 1u) {
-          stg[pos] = v[u];
-          sidx[pos] = gbase + u * kSelThreads;
-          ++pos;
-        }
-      }
-      __syncwarp();
-      for (int e0 = 0; e0 < 8 * tot; e0 += 32) {
-        const int e = e0 + lane;
-        bool p = false;
-        unsigned long long key = 0;
-        if (e < 8 * tot) {
-          const unsigned b = stg16[e];
-          if ((b & 0x7FFFu) >= tkey) {
-            key = make_key(b, (unsigned)(a0 + 8 * sidx[e >> 3] + (e & 7)));
-            p = key >= theta;
-          }
-        }
-        warp_append(p, key, wb, cnt, theta, kk, lane);
+    for (int u = 0; u < kSelU; ++u) {
+      if ((hm >> u) & 1u) {
+        if (STAGE) w.stg[pos] = v[u];
+        w.sidx[pos] = gbase + u * kSelThreads;
+        ++pos;
       }
     }
-    if (lane == 0) s.wcnt[warp] = cnt;
-    __syncthreads();
+    __syncwarp();
+    if (STAGE) {
+      const uint16_t* stg16 = reinterpret_cast<const uint16_t*>(w.stg);
+      test_flagged(tot, a0, w, kk, lane, [&](int e) { return (unsigned)stg16[e]; });
+    } else {
+      const uint16_t* el = cg.base + a0;
+      test_flagged(tot, a0, w, kk, lane, [&](int e) { return (unsigned)el[8 * w.sidx[e >> 3] + (e & 7)]; });
+    }
+  }
+}
+
+#if TL_RING
+// Ring consumer: this warp's share (vectors warp*128 + u*32 + lane) of every stage
+// of the chunk, in the producer's order.  Flagged elements are read straight from
+// the stage, which is released to the producer afterwards.
+struct Ring {
+  const uint4* stages;           // [kRingStages][kTileVec]
+  unsigned long long* full;      // [kRingStages] producer -> consumers
+  unsigned long long* empty;     // [kRingStages] consumers -> producer (count = consumer warps)
+  uint32_t seq;                  // stages consumed by this warp
+};
+__device__ __forceinline__ void pass_ring(const ChunkGeo& cg, WarpScan& w, Ring& r, int kk, int warp, int lane) {
+  const int nvec = cg.nvec, a0 = cg.a0;
+  const int q0 = warp * (kTileVec / kSelWarps) + lane;
+  for (int st = 0; st < cg.nst; ++st) {
+    const uint32_t slot = r.seq % kRingStages;
+    mbar_wait(r.full + slot, (r.seq / kRingStages) & 1u);
+    const uint4* __restrict__ stage = r.stages + (size_t)slot * kTileVec;
+    const int g0 = st * kTileVec;  // vector id of stage slot 0
+    unsigned mu[kSelU];
+#pragma unroll
+    for (int u = 0; u < kSelU; ++u) {
+      const uint4 v = g0 + q0 + u * 32 < nvec ? stage[q0 + u * 32] : make_uint4(0u, 0u, 0u, 0u);
+      mu[u] = hmaxabs2(hmaxabs2(v.x, v.y), hmaxabs2(v.z, v.w));
+    }
+    unsigned m = mu[0];
+#pragma unroll
+    for (int u = 1; u < kSelU; ++u) m = hmaxabs2(m, mu[u]);
+    const unsigned c2 = coarse_c2(w.theta, (unsigned)(a0 + st * kTileElems));
+    const bool hit = coarse_hit(m, c2);
+    if (__any_sync(0xFFFFFFFFu, hit)) {
+      // u-major list of flagged stage slots (ballots only)
+      const unsigned lt = lanemask_lt();
+      int tot = 0;
+#pragma unroll
+      for (int u = 0; u < kSelU; ++u) {
+        const bool f = hit && g0 + q0 + u * 32 < nvec && coarse_hit(mu[u], c2);
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, f);
+        if (f) w.sidx[tot + __popc(bal & lt)] = q0 + u * 32;
+        tot += __popc(bal);
+      }
+      __syncwarp();
+      const uint16_t* st16 = reinterpret_cast<const uint16_t*>(stage);
+      const int a0s = a0 + 8 * g0;  // element index of stage slot 0
+      test_flagged(tot, a0s, w, kk, lane, [&](int e) { return (unsigned)st16[w.sidx[e >> 3] * 8 + (e & 7)]; });
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(r.empty + slot);
+    ++r.seq;
+  }
+}
+
+// Producer warp: stream every chunk of this CTA, stage by stage, into the ring.
+__device__ void ring_producer(const SelArgs& a, uint4* stages, unsigned long long* full,
+                              unsigned long long* empty, int lane) {
+  uint32_t seq = 0;
+  for (int64_t j = blockIdx.x; j < a.n_chunks; j += gridDim.x) {
+    const ChunkGeo g = chunk_geo(a, j);
+    const uint4* src = reinterpret_cast<const uint4*>(g.base + g.a0);
+    for (int st = 0; st < g.nst; ++st, ++seq) {
+      const uint32_t slot = seq % kRingStages;
+      if (seq >= (uint32_t)kRingStages) mbar_wait(empty + slot, ((seq / kRingStages) - 1u) & 1u);
+      if (lane == 0) {
+        const uint32_t bytes = (uint32_t)min(kTileVec, g.nvec - st * kTileVec) * 16u;
+        mbar_expect_tx(full + slot, bytes);
+        bulk_g2s(stages + (size_t)slot * kTileVec, src + (size_t)st * kTileVec, bytes, full + slot);
+      }
+      __syncwarp();
+    }
+  }
+}
+#endif
+
+// Top-kk of chunk cg -> s.out[0..kk) in rank order.  s.theta holds this chunk's
+// speculative threshold on entry.  Consumer threads only; ends with a barrier.
+template <typename Src>
+__device__ void select_chunk(const ChunkGeo& cg, int kk, SelState& s, Src& src) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  WarpScan w;
+  w.wb = s.wbuf[warp];
+  w.sidx = s.sidx[warp];
+#if TL_RING
+  w.stg = nullptr;
+#else
+  w.stg = s.stage[warp];
+#endif
+  const int tail0 = cg.a0 + (cg.nvec << 3);
+  int total;
+  bool first_pass = true;
+  for (;;) {
+    w.theta = s.theta;
+    w.cnt = 0;
+    const bool spec = w.theta != 0ull;
+    if (warp == 0) {  // scalar head / tail elements (chunks not 16-B aligned)
+      bool p = false;
+      unsigned long long key = 0;
+      if (lane < cg.a0) {
+        key = make_key(cg.base[lane], lane);
+        p = key >= w.theta;
+      } else if (lane >= 8 && lane - 8 < cg.n - tail0) {
+        key = make_key(cg.base[tail0 + lane - 8], tail0 + lane - 8);
+        p = key >= w.theta;
+      }
+      warp_append(p, key, w.wb, w.cnt, w.theta, kk, lane);
+    }
+#if TL_RING
+    if (first_pass) pass_ring(cg, w, src, kk, warp, lane);
+    else pass_ldg<false>(cg, w, kk, warp, lane);
+#else
+    pass_ldg<true>(cg, w, kk, warp, lane);
+#endif
+    first_pass = false;
+    if (lane == 0) s.wcnt[warp] = w.cnt;
+    csync();
     total = 0;
 #pragma unroll
-    for (int w = 0; w < kSelWarps; ++w) total += s.wcnt[w];
+    for (int q = 0; q < kSelWarps; ++q) total += s.wcnt[q];
     if (total >= kk) break;
-    // the speculative theta excluded part of the top-kk: redo the chunk exactly
+    // the speculative theta excluded part of the top-kk: re-scan exactly
     if (!spec) __trap();  // unreachable: theta = 0 admits every element
-    __syncthreads();
+    csync();
     if (tid == 0) {
       s.theta = 0ull;
       s.delta = min(s.delta + 4, 0x4000);
     }
-    __syncthreads();
+    csync();
   }
 
   if (total <= 256) {
@@ -434,13 +623,13 @@ __device__ void select_chunk(const uint16_t* __restrict__ base, int n, int kk, S
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const int q = r * 32 + lane;
-        int run = 0, w = 0, basew = 0;
+        int run = 0, ww = 0, basew = 0;
 #pragma unroll
         for (int t = 0; t < kSelWarps; ++t) {  // segment of q in the concatenated warp buffers
-          if (q >= run) { w = t; basew = run; }
+          if (q >= run) { ww = t; basew = run; }
           run += s.wcnt[t];
         }
-        a[r] = q < total ? s.wbuf[w][q - basew] : 0ull;
+        a[r] = q < total ? s.wbuf[ww][q - basew] : 0ull;
       }
       warp_bitonic_desc<8>(a, lane);
 #pragma unroll
@@ -448,9 +637,9 @@ __device__ void select_chunk(const uint16_t* __restrict__ base, int n, int kk, S
         if (r * 32 + lane < kk) s.out[r * 32 + lane] = a[r];
     }
   } else {
-    rank_many(kk, total, s);
+    rank_many(kk, s);
   }
-  __syncthreads();
+  csync();
   if (tid == 0) {  // speculation for this CTA's next chunk
     int d = s.delta;
     if (total > kk + 128 && d > 1) --d;
@@ -461,12 +650,47 @@ __device__ void select_chunk(const uint16_t* __restrict__ base, int n, int kk, S
   }
 }
 
-__device__ __forceinline__ void sel_init(SelState& s) {
+struct NoSrc {};
+#if TL_RING
+using SelSrc = Ring;
+#else
+using SelSrc = NoSrc;
+#endif
+
+// Carve shared memory; the producer warp (TL_RING) streams and returns false,
+// consumer threads get their ring view and return true.
+__device__ __forceinline__ bool sel_setup(uint8_t* smem, const SelArgs& a, SelState*& sp, SelSrc& src) {
+  SelState& s = *reinterpret_cast<SelState*>(smem);
+  sp = &s;
   if (threadIdx.x == 0) {
     s.theta = 0;
     s.delta = 8;
   }
+#if TL_RING
+  uint4* stages = reinterpret_cast<uint4*>(smem + kSelStateBytes);
+  unsigned long long* full =
+      reinterpret_cast<unsigned long long*>(smem + kSelStateBytes + (size_t)kRingStages * kRingStageBytes);
+  unsigned long long* empty = full + kRingStages;
+  if (threadIdx.x < kRingStages) {
+    mbar_init(full + threadIdx.x, 1);
+    mbar_init(empty + threadIdx.x, kSelWarps);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
+  if (threadIdx.x >= kSelThreads) {
+    ring_producer(a, stages, full, empty, threadIdx.x & 31);
+    return false;
+  }
+  src.stages = stages;
+  src.full = full;
+  src.empty = empty;
+  src.seq = 0;
+#else
+  (void)a;
+  (void)src;
+  __syncthreads();
+#endif
+  return true;
 }
 
 // ----------------------------------------------------------------------------- kernels
@@ -508,18 +732,19 @@ __global__ void chunk_prefix_kernel(const int64_t* __restrict__ row_off, int n_r
   }
 }
 
-__global__ void __launch_bounds__(kSelThreads, kSelMinBlocks)
-prove_select_kernel(const uint16_t* __restrict__ hidden, const int64_t* __restrict__ row_off,
-                    const int64_t* __restrict__ prefix, int n_roll, int H, int C, int K,
-                    int64_t n_chunks, int32_t* __restrict__ idx_out, uint16_t* __restrict__ bits_out) {
-  __shared__ SelState s;
-  sel_init(s);
-  const int64_t total = prefix[n_roll];
-  for (int64_t j = blockIdx.x; j < n_chunks && j < total; j += gridDim.x) {
-    const ChunkRef cr = locate_chunk(prefix, row_off, n_roll, j, C);
-    const int n = cr.rows * H;
-    const int kk = min(K, n);
-    select_chunk(hidden + cr.row_start * (int64_t)H, n, kk, s);
+__global__ void __launch_bounds__(kSelBlockThreads, kSelMinBlocks)
+prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restrict__ bits_out) {
+  extern __shared__ __align__(128) uint8_t sel_smem[];
+  a.n_chunks = min(a.n_chunks, a.prefix[a.n_roll]);
+  SelState* sp;
+  SelSrc src;
+  if (!sel_setup(sel_smem, a, sp, src)) return;  // producer warp done
+  SelState& s = *sp;
+  const int K = a.K;
+  for (int64_t j = blockIdx.x; j < a.n_chunks; j += gridDim.x) {
+    const ChunkGeo g = chunk_geo(a, j);
+    const int kk = min(K, g.n);
+    select_chunk(g, kk, s, src);
     for (int i = threadIdx.x; i < K; i += kSelThreads) {
       if (i < kk) {
         const unsigned long long v = s.out[i];
@@ -530,7 +755,7 @@ prove_select_kernel(const uint16_t* __restrict__ hidden, const int64_t* __restri
         bits_out[j * K + i] = 0;
       }
     }
-    __syncthreads();
+    csync();
   }
 }
 
@@ -751,21 +976,22 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
   }
 }
 
-__global__ void __launch_bounds__(kSelThreads, kSelMinBlocks)
-verify_kernel(const uint16_t* __restrict__ hidden, const int64_t* __restrict__ row_off,
-              const int64_t* __restrict__ prefix, int n_roll, int H, int C, int K, int64_t n_chunks,
-              const uint8_t* __restrict__ proofs, tl_thresholds th,
+__global__ void __launch_bounds__(kSelBlockThreads, kSelMinBlocks)
+verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
               tl_chunk_stats* __restrict__ stats_out, uint8_t* __restrict__ accept_out) {
-  __shared__ SelState s;
-  sel_init(s);
+  extern __shared__ __align__(128) uint8_t sel_smem[];
+  a.n_chunks = min(a.n_chunks, a.prefix[a.n_roll]);
+  SelState* sp;
+  SelSrc src;
+  if (!sel_setup(sel_smem, a, sp, src)) return;  // producer warp done
+  SelState& s = *sp;
   const int tid = threadIdx.x;
+  const int K = a.K;
   const int PB = 2 + 2 * K;
-  const int64_t total = prefix[n_roll];
-  for (int64_t j = blockIdx.x; j < n_chunks && j < total; j += gridDim.x) {
-    const ChunkRef cr = locate_chunk(prefix, row_off, n_roll, j, C);
-    const int n = cr.rows * H;
-    const int kk = min(K, n);
-    select_chunk(hidden + cr.row_start * (int64_t)H, n, kk, s);
+  for (int64_t j = blockIdx.x; j < a.n_chunks; j += gridDim.x) {
+    const ChunkGeo g = chunk_geo(a, j);
+    const int kk = min(K, g.n);
+    select_chunk(g, kk, s, src);
 
     const uint8_t* pr = proofs + j * PB;
     if (tid == 0) {
@@ -774,22 +1000,23 @@ verify_kernel(const uint16_t* __restrict__ hidden, const int64_t* __restrict__ r
     }
     for (int i = tid; i < K; i += kSelThreads) s.coef[i] = (uint16_t)(((unsigned)pr[2 + 2 * i] << 8) | pr[3 + 2 * i]);
     if (tid < 128) s.mhist[tid] = 0;
-    __syncthreads();
+    csync();
     const unsigned p = s.p;
     const bool bad = p < 2;
     // Horner split over the two halves of the block: thread t < 128 evaluates
     // c_0..c_{h-1} at point t, thread t + 128 evaluates c_h..c_{K-1} and scales by x^h
-    const int pt = tid & 127, half = tid >> 7, h = (K + 1) >> 1;
+    const int pt = tid & 127, half = (tid >> 7) & 1, h = (K + 1) >> 1;
+    const bool horner = tid < 256 && pt < kk;
     uint32_t acc = 0, x = 0;
-    if (!bad && pt < kk) {
+    if (!bad && horner) {
       const ModP m(p);
       x = m.red(key_idx(s.out[pt]));
       const int k_lo = half ? h : 0, k_hi = half ? K : h;
       for (int k = k_hi - 1; k >= k_lo; --k) acc = m.red(acc * x + (uint32_t)s.coef[k]);
       if (half) s.hpart[pt] = m.mul(acc, m.pow(x, (uint32_t)h));
     }
-    __syncthreads();
-    if (!bad && half == 0 && pt < kk) {
+    csync();
+    if (!bad && horner && half == 0) {
       const ModP m(p);
       const unsigned long long v = s.out[pt];
       const uint32_t claimed = m.add(acc, s.hpart[pt]);
@@ -804,7 +1031,7 @@ verify_kernel(const uint16_t* __restrict__ hidden, const int64_t* __restrict__ r
         atomicAdd(&s.nmatch, 1u);
       }
     }
-    __syncthreads();
+    csync();
     if (tid < 32) {  // median over the 128-bin histogram of |mantissa diff|
       const unsigned nm = s.nmatch;
       unsigned c4[4], sum = 0;
@@ -854,7 +1081,7 @@ verify_kernel(const uint16_t* __restrict__ hidden, const int64_t* __restrict__ r
         accept_out[j] = (uint8_t)(st.flags & TL_STAT_ACCEPT);
       }
     }
-    __syncthreads();
+    csync();
   }
 }
 
@@ -993,7 +1220,8 @@ int sm_count() {
 
 int sel_grid(int64_t n_chunks, const void* kernel) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSelThreads, 0) != cudaSuccess || per_sm < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSelBlockThreads, kSelSmem) != cudaSuccess ||
+      per_sm < 1)
     per_sm = 1;
   const int64_t g = (int64_t)sm_count() * per_sm;
   return (int)(n_chunks < g ? (n_chunks > 0 ? n_chunks : 1) : g);
@@ -1047,8 +1275,12 @@ int tl_select(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, in
   int64_t* prefix = reinterpret_cast<int64_t*>(ws + L.prefix);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix);
-  prove_select_kernel<<<sel_grid(n_chunks, (const void*)prove_select_kernel), kSelThreads, 0, st>>>(
-      hidden, row_off, prefix, n_roll, H, C, K, n_chunks, idx_out, bits_out);
+  const SelArgs a{hidden, row_off, prefix, n_roll, H, C, K, n_chunks};
+  if (cudaFuncSetAttribute(prove_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
+      cudaSuccess)
+    return TL_ECUDA;
+  prove_select_kernel<<<sel_grid(n_chunks, (const void*)prove_select_kernel), kSelBlockThreads, kSelSmem, st>>>(
+      a, idx_out, bits_out);
   return launch_status();
 }
 
@@ -1108,9 +1340,14 @@ int tl_verify(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, in
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
   chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix);
-  if (n_chunks > 0)
-    verify_kernel<<<sel_grid(n_chunks, (const void*)verify_kernel), kSelThreads, 0, st>>>(
-        hidden, row_off, prefix, n_roll, H, C, K, n_chunks, proofs, *thresholds_host, stats_out, accept);
+  if (n_chunks > 0) {
+    const SelArgs a{hidden, row_off, prefix, n_roll, H, C, K, n_chunks};
+    if (cudaFuncSetAttribute(verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
+        cudaSuccess)
+      return TL_ECUDA;
+    verify_kernel<<<sel_grid(n_chunks, (const void*)verify_kernel), kSelBlockThreads, kSelSmem, st>>>(
+        a, proofs, *thresholds_host, stats_out, accept);
+  }
   if (rollout_accept_out)
     rollout_verdict_kernel<<<(n_roll + 7) / 8, 256, 0, st>>>(accept, prefix, n_roll, rollout_accept_out);
   return launch_status();
