@@ -233,3 +233,24 @@ def test_api_argument_errors():
         api.ToplocEngine(topk=129)
     with pytest.raises(ValueError):
         api.ToplocEngine(chunk=0)
+
+
+def test_toploc_on_reference_forge_corpus():
+    """TOPLOC prove / verify on the reference's own activations (tests/golden/forge_*,
+    produced by swarm's Forge): honest records verify, GPU stats and verdicts equal
+    the oracle's for every record, at default and exact thresholds."""
+    from paper_2505_07291_b200.swarm_adapter import to_bf16_bits
+    with open(os.path.join(GOLDEN, "forge_golden.json")) as f:
+        meta = json.load(f)
+    arrays = np.load(os.path.join(GOLDEN, "forge_golden.npz"))
+    eng = api.engine()
+    for th in (api.Thresholds(), api.Thresholds(0, 0.0, 0.0))[:]:
+        for m in meta:
+            prv = to_bf16_bits(arrays[f"prv_{m['i']}"])
+            val = to_bf16_bits(arrays[f"val_{m['i']}"])
+            offs = [0, prv.shape[0]]
+            pb = gpu_prove(prv, offs)
+            assert pb.to_bytes() == TO.build_proofs(prv, offs)
+            vb, ost, over = check_verify_against_oracle(val, offs, flat_proofs(pb), th)
+            if m["kind"] == "honest":
+                assert over == [True]

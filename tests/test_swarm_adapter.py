@@ -1,0 +1,128 @@
+"""The swarm adapter against the reference's own validator (CPU, where the
+reference package is importable: PYTHONPATH or /root/reference/pkg/src).
+
+The adapter's backend is injected: the GPU kernels are parity-tested against the
+oracle in tests/test_gpu_parity.py, so here the oracle stands in for them to test
+the adapter's wiring through the reference's real control flow
+(swarm/validator/checks.py:154-215, swarm/validator/adversaries.py)."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+REF = "/root/reference/pkg/src"
+if os.path.isdir(REF) and REF not in sys.path:
+    sys.path.append(REF)
+swarm = pytest.importorskip("swarm")
+
+from oracle import exact_oracle as EO  # noqa: E402
+from oracle import toploc_oracle as TO  # noqa: E402
+from paper_2505_07291_b200 import swarm_adapter  # noqa: E402
+from paper_2505_07291_b200.api import Thresholds  # noqa: E402
+
+
+class OracleBackend:
+    def build_commitments(self, hidden, k):
+        return EO.build_commitments(hidden, k)
+
+    def prove(self, bits, k):
+        return TO.build_proofs(bits, [0, bits.shape[0]], C=k)[0]
+
+    def verify(self, bits, proofs, k, th):
+        _, ok = TO.verify_proofs(bits, [0, bits.shape[0]], [proofs], C=k,
+                                 th=TO.Thresholds(th.max_exp_mismatch, th.max_mant_mean, th.max_mant_median))
+        return ok[0]
+
+
+def fixtures():
+    from swarm.config import TOY_MODEL
+    from swarm.keys import SigningKey
+    from swarm.policy import init_params
+    from swarm.tasks import generate_dataset
+    from swarm.validator import CheckContext
+    from swarm.validator.adversaries import Forge
+    dataset = generate_dataset(seed=10, n=64)
+    params = init_params(TOY_MODEL, seed=2, scale=1.0)
+    stale = params.copy()
+    rng = np.random.default_rng(3)
+    for a in stale.arrays():
+        a += rng.normal(0, 1e-3, a.shape)
+    other = init_params(TOY_MODEL, seed=77, scale=1.0)
+    forge = Forge(params=params, stale_params=stale, other_params=other, mcfg=TOY_MODEL, dataset=dataset,
+                  key=SigningKey.from_seed(7, 0), checkpoint_version=5)
+    ctx = CheckContext(mcfg=TOY_MODEL, dataset=dataset, alpha=0.01, budgets=(8, 16, 24, 32), group_size=4,
+                       p_low=0.005, load_checkpoint=lambda v: {5: params, 2: stale}.get(v))
+    return forge, ctx
+
+
+@pytest.fixture
+def adapter():
+    yield swarm_adapter
+    swarm_adapter.uninstall()
+
+
+def validate(blob, ctx):
+    import swarm.validator.checks as checks
+    return checks.validate_file(blob, ctx)
+
+
+def test_exact_mode_is_byte_identical_and_keeps_verdicts(adapter):
+    import swarm.worker.rollout as rollout
+    forge, ctx = fixtures()
+    orig = rollout.build_commitments
+    h = np.random.default_rng(0).normal(size=(70, 8))
+    adapter.install("exact", backend=OracleBackend())
+    assert rollout.build_commitments is not orig
+    assert rollout.build_commitments(h) == orig(h)
+    for step in (1, 2):
+        assert validate(forge.honest(step, 0), ctx).result == "accept"
+        v = validate(forge.generate("wrong-model", step, 0), ctx)
+        assert (v.result, v.failed_check) == ("reject", "commitment")
+    adapter.uninstall()
+    assert rollout.build_commitments is orig
+
+
+def test_toploc_mode_wire_format(adapter):
+    from swarm.worker.files import parse_rollout_file
+    forge, ctx = fixtures()
+    adapter.install("toploc", backend=OracleBackend())
+    f = parse_rollout_file(forge.honest(3, 0))
+    for rec in f.records:
+        assert len(rec.commitments) == -(-len(rec.output_tokens) // f.commit_interval)
+        assert all(len(c) == 2 * 258 for c in rec.commitments)
+
+
+@pytest.mark.parametrize("attack", ["malformed-file", "cherry-picked-prompt", "forged-reward", "early-eos",
+                                    "token-substitution"])
+def test_toploc_mode_keeps_reference_check_order(adapter, attack):
+    from swarm.validator.adversaries import EXPECTED_CHECK
+    forge, ctx = fixtures()
+    adapter.install("toploc", backend=OracleBackend())
+    assert validate(forge.honest(2, 0), ctx).result == "accept"
+    v = validate(forge.generate(attack, 2, 0), ctx)
+    assert (v.result, v.failed_check) == ("reject", EXPECTED_CHECK[attack])
+
+
+def test_toploc_mode_commitment_verdicts(adapter):
+    """Honest files pass; a tampered proof and an unrelated model are rejected at
+    the commitment check.  The reference's 'wrong-model' forgery (a checkpoint
+    within 1e-3 of the claimed one) is within TOPLOC's tolerance at the default
+    thresholds (accept) and rejected at exact thresholds."""
+    from swarm.worker.files import build_rollout_file, parse_rollout_file
+    forge, ctx = fixtures()
+    adapter.install("toploc", backend=OracleBackend())
+    for step in (1, 2, 3):
+        assert validate(forge.honest(step, 0), ctx).result == "accept"
+    f = parse_rollout_file(forge.honest(4, 0))
+    p = bytearray(bytes.fromhex(f.records[1].commitments[0]))
+    p[0:2] = (65479).to_bytes(2, "big")                    # wrong modulus -> garbage evaluations
+    f.records[1].commitments[0] = bytes(p).hex()
+    v = validate(build_rollout_file(f, forge.key), ctx)
+    assert (v.result, v.failed_check) == ("reject", "commitment") and "record 1" in v.details
+    wm = forge.generate("wrong-model", 1, 0)
+    assert validate(wm, ctx).result == "accept"
+    adapter.install("toploc", thresholds=Thresholds(0, 0.0, 0.0), backend=OracleBackend())
+    v = validate(wm, ctx)
+    assert (v.result, v.failed_check) == ("reject", "commitment")
