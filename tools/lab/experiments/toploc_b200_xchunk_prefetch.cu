@@ -41,8 +41,8 @@ constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kWarpCap = 256;                 // per-warp candidate buffer (2 KiB)
 static_assert(kWarpCap >= TL_MAX_K + 32, "a compaction must leave room for one full ballot");
 constexpr int kStageVec = 32 * kSelU;         // per-warp flagged-vector list (every vector of a batch)
-#ifndef TL_SPEC_HIST
-#define TL_SPEC_HIST 2  // speculation = min over the last TL_SPEC_HIST kk-th magnitudes (power of 2)
+#ifndef TL_XPF
+#define TL_XPF 0  // prefetch the next chunk's first tile across the chunk tail (spills at 64 regs)
 #endif
 #ifndef TL_RING_STAGES
 #define TL_RING_STAGES 5
@@ -157,7 +157,7 @@ struct SelState {
 #endif
   unsigned long long out[TL_MAX_K];              // selected keys, rank order
   unsigned long long theta;                      // chunk-start threshold (speculation)
-  unsigned khist[TL_SPEC_HIST];                  // last kk-th magnitudes (speculation history)
+  unsigned khist[4];                             // last kk-th magnitudes (speculation history)
   int khead;
   int retry;                                     // re-scans of the current chunk
   int wcnt[kSelWarps];
@@ -434,15 +434,24 @@ __device__ __forceinline__ void test_flagged(int nflag, int a0, WarpScan& w, int
 // t: t*1024 + u*256 + warp*32 + lane.  Flagged vectors are copied to w.stg
 // (STAGE) or their elements re-read from global memory (L2-hot; the TL_RING
 // restart path, which has no staging buffer).
-template <bool STAGE>
-__device__ __forceinline__ void pass_ldg(const ChunkGeo& cg, WarpScan& w, int kk, int warp, int lane) {
+// Registers carrying the first tile of the CTA's next chunk across the chunk-end
+// tail (barrier, ranking, emit), so every warp keeps loads in flight there.
+struct Prefetch {
+  uint4 v[kSelU];
+  bool valid;
+};
+
+template <bool STAGE, bool PF>
+__device__ __forceinline__ void pass_ldg(const ChunkGeo& cg, WarpScan& w, int kk, int warp, int lane,
+                                         Prefetch& pf, const ChunkGeo& next, bool has_next) {
   const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(cg.base + cg.a0);
   const int nvec = cg.nvec, a0 = cg.a0;
   uint4 vn[kSelU];
 #pragma unroll
   for (int u = 0; u < kSelU; ++u) {
     const int g = warp * 32 + lane + u * kSelThreads;
-    vn[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
+    if (PF && pf.valid) vn[u] = pf.v[u];
+    else vn[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
   }
   for (int it = 0; it < cg.nst; ++it) {
     const int gbase = it * kTileVec + warp * 32 + lane;
@@ -492,6 +501,17 @@ __device__ __forceinline__ void pass_ldg(const ChunkGeo& cg, WarpScan& w, int kk
     } else {
       const uint16_t* el = cg.base + a0;
       test_flagged(tot, a0, w, kk, lane, [&](int e) { return (unsigned)el[8 * w.sidx[e >> 3] + (e & 7)]; });
+    }
+  }
+  if (PF) {  // issue the next chunk's first tile before this chunk's tail
+    pf.valid = has_next;
+    if (has_next) {
+      const uint4* __restrict__ nb = reinterpret_cast<const uint4*>(next.base + next.a0);
+#pragma unroll
+      for (int u = 0; u < kSelU; ++u) {
+        const int g = warp * 32 + lane + u * kSelThreads;
+        pf.v[u] = g < next.nvec ? ld_stream(nb + g) : make_uint4(0u, 0u, 0u, 0u);
+      }
     }
   }
 }
@@ -571,7 +591,8 @@ __device__ void ring_producer(const SelArgs& a, uint4* stages, unsigned long lon
 // Top-kk of chunk cg -> s.out[0..kk) in rank order.  s.theta holds this chunk's
 // speculative threshold on entry.  Consumer threads only; ends with a barrier.
 template <typename Src>
-__device__ void select_chunk(const ChunkGeo& cg, int kk, SelState& s, Src& src) {
+__device__ __forceinline__ void select_chunk(const ChunkGeo& cg, int kk, SelState& s, Src& src, Prefetch& pf,
+                                             const ChunkGeo& next, bool has_next) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   WarpScan w;
   w.wb = s.wbuf[warp];
@@ -602,9 +623,16 @@ __device__ void select_chunk(const ChunkGeo& cg, int kk, SelState& s, Src& src) 
     }
 #if TL_RING
     if (first_pass) pass_ring(cg, w, src, kk, warp, lane);
-    else pass_ldg<false>(cg, w, kk, warp, lane);
+    else pass_ldg<false, false>(cg, w, kk, warp, lane, pf, next, false);
 #else
-    pass_ldg<true>(cg, w, kk, warp, lane);
+    if (first_pass) {
+      pass_ldg<true, (TL_XPF != 0)>(cg, w, kk, warp, lane, pf, next, has_next);
+    } else {
+#pragma unroll
+      for (int u = 0; u < kSelU; ++u) pf.v[u] = make_uint4(0u, 0u, 0u, 0u);
+      pf.valid = false;
+      pass_ldg<true, false>(cg, w, kk, warp, lane, pf, next, false);
+    }
 #endif
     first_pass = false;
     if (lane == 0) s.wcnt[warp] = w.cnt;
@@ -650,15 +678,13 @@ __device__ void select_chunk(const ChunkGeo& cg, int kk, SelState& s, Src& src) 
     rank_many(kk, s);
   }
   csync();
-  if (tid == 0) {  // speculation for this CTA's next chunk
+  if (tid == 0) {  // speculation for this CTA's next chunk: min of the last 4 kk-th magnitudes - delta
     int d = s.delta;
     if (total > kk + 128 && d > 1) --d;
     else if (total < kk + 32) ++d;
     s.delta = d;
-    s.khist[s.khead++ & (TL_SPEC_HIST - 1)] = (unsigned)(s.out[kk - 1] >> 40);
-    unsigned kmag = s.khist[0];
-#pragma unroll
-    for (int q = 1; q < TL_SPEC_HIST; ++q) kmag = min(kmag, s.khist[q]);  // min of the last kk-th magnitudes
+    s.khist[s.khead++ & 3] = (unsigned)(s.out[kk - 1] >> 40);
+    const unsigned kmag = min(min(s.khist[0], s.khist[1]), min(s.khist[2], s.khist[3]));
     s.theta = kmag > (unsigned)d ? ((unsigned long long)(kmag - (unsigned)d) << 40) : 0ull;
     s.retry = 0;
   }
@@ -681,7 +707,7 @@ __device__ __forceinline__ bool sel_setup(uint8_t* smem, const SelArgs& a, SelSt
     s.delta = 8;
     s.khead = 0;
     s.retry = 0;
-    for (int i = 0; i < TL_SPEC_HIST; ++i) s.khist[i] = 0x7FFFu;
+    for (int i = 0; i < 4; ++i) s.khist[i] = 0x7FFFu;
   }
 #if TL_RING
   uint4* stages = reinterpret_cast<uint4*>(smem + kSelStateBytes);
@@ -758,10 +784,14 @@ prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restri
   if (!sel_setup(sel_smem, a, sp, src)) return;  // producer warp done
   SelState& s = *sp;
   const int K = a.K;
+  Prefetch pf;
+  pf.valid = false;
+  ChunkGeo g = chunk_geo(a, blockIdx.x < a.n_chunks ? (int64_t)blockIdx.x : 0);
   for (int64_t j = blockIdx.x; j < a.n_chunks; j += gridDim.x) {
-    const ChunkGeo g = chunk_geo(a, j);
+    const bool has_next = j + gridDim.x < a.n_chunks;
+    const ChunkGeo gn = chunk_geo(a, has_next ? j + gridDim.x : j);
     const int kk = min(K, g.n);
-    select_chunk(g, kk, s, src);
+    select_chunk(g, kk, s, src, pf, gn, has_next);
     for (int i = threadIdx.x; i < K; i += kSelThreads) {
       if (i < kk) {
         const unsigned long long v = s.out[i];
@@ -773,6 +803,7 @@ prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restri
       }
     }
     csync();
+    g = gn;
   }
 }
 
@@ -1005,10 +1036,14 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
   const int tid = threadIdx.x;
   const int K = a.K;
   const int PB = 2 + 2 * K;
+  Prefetch pf;
+  pf.valid = false;
+  ChunkGeo g = chunk_geo(a, blockIdx.x < a.n_chunks ? (int64_t)blockIdx.x : 0);
   for (int64_t j = blockIdx.x; j < a.n_chunks; j += gridDim.x) {
-    const ChunkGeo g = chunk_geo(a, j);
+    const bool has_next = j + gridDim.x < a.n_chunks;
+    const ChunkGeo gn = chunk_geo(a, has_next ? j + gridDim.x : j);
     const int kk = min(K, g.n);
-    select_chunk(g, kk, s, src);
+    select_chunk(g, kk, s, src, pf, gn, has_next);
 
     const uint8_t* pr = proofs + j * PB;
     if (tid == 0) {
@@ -1099,6 +1134,7 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
       }
     }
     csync();
+    g = gn;
   }
 }
 
