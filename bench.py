@@ -220,6 +220,20 @@ def run_b200(args, cfg, rank, world, local_rank):
         step()
     torch.cuda.synchronize(dev)
 
+    # serial per-phase times (informational: kernels run back to back, 4 CTAs/SM)
+    ser = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(5)]
+    for e in ser:
+        e[0].record(stream)
+        plan.select(prv)
+        e[1].record(stream)
+        plan.commit()
+        e[2].record(stream)
+        plan.verify(val)
+        e[3].record(stream)
+    torch.cuda.synchronize(dev)
+    serial_ms = {k: sum(e[i].elapsed_time(e[i + 1]) for e in ser) / len(ser)
+                 for i, k in enumerate(("select", "commit", "verify"))}
+
     # spot-check bit-exactness at full size on sampled chunks (outside the timed region)
     spot = None
     if args.spot_check and rank == 0:
@@ -237,34 +251,59 @@ def run_b200(args, cfg, rank, world, local_rank):
             okp.append(pr[0] == got[j].tobytes())
         spot = {"chunks": js, "proofs_bit_exact": all(okp)}
 
+    pipe = api.Pipeline(eng, offs, H, ctas_per_sm=args.ctas) if args.pipeline else None
+    if pipe is not None:
+        pipe.run([prv] * args.warmup, [val] * args.warmup)
+        torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    sel_ev, ver_ev = {}, {}
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record(stream)
-    for k in range(args.steps):
-        e = evs[k]
-        e[0].record(stream)
-        plan.select(prv)
-        e[1].record(stream)
-        plan.commit()
-        e[2].record(stream)
-        plan.verify(val)
-        e[3].record(stream)
-    t_end.record(stream)
-    torch.cuda.synchronize(dev)
+    if pipe is not None:
+        def mark(store):
+            def f(k, what, st):
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(st)
+                store.setdefault(k, {})[what] = ev
+            return f
+        t_start.record(stream)
+        outs = pipe.run([prv] * args.steps, [val] * args.steps, on_select=mark(sel_ev), on_verify=mark(ver_ev))
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+        sel_ms = sum(v["start"].elapsed_time(v["end"]) for v in sel_ev.values()) / args.steps
+        ver_ms = sum(v["start"].elapsed_time(v["end"]) for v in ver_ev.values()) / args.steps
+        com_ms = serial_ms["commit"]
+        accepted = int(outs[-1].sum().item())
+        assert all(int(o.sum().item()) == accepted for o in outs)
+        spot_pipe = bool(torch.equal(pipe.plans[(args.steps - 1) % 2].proofs, plan.proofs))
+        if spot is not None:
+            spot["pipeline_proofs_equal_serial"] = spot_pipe
+    else:
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+        t_start.record(stream)
+        for k in range(args.steps):
+            e = evs[k]
+            e[0].record(stream)
+            plan.select(prv)
+            e[1].record(stream)
+            plan.commit()
+            e[2].record(stream)
+            plan.verify(val)
+            e[3].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+        sel_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+        com_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+        ver_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+        accepted = int(plan.rollout_accept.sum().item())
     clk = clocks.stop()
     elapsed_ms = t_start.elapsed_time(t_end)
-    sel_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    com_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
-    ver_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
 
-    accepted = int(plan.rollout_accept.sum().item())
     # max over ranks (device-timed)
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
     gather_ms = None
@@ -359,7 +398,10 @@ def run_b200(args, cfg, rank, world, local_rank):
                               "achieved_gbs": value / world * algorithmic_bytes_per_token(H) / 1e9,
                               "frac": value / world * algorithmic_bytes_per_token(H) / 1e9 / peak},
             "phases_ms": {"select": sel_ms, "commit": com_ms, "verify": ver_ms,
-                          "verify_gbs": ver_bytes / (ver_ms / 1e3) / 1e9, "verdict_gather": gather_ms},
+                          "verify_gbs": ver_bytes / (ver_ms / 1e3) / 1e9, "verdict_gather": gather_ms,
+                          "serial": serial_ms,
+                          "schedule": (f"pipelined: commit(k) on a side stream overlaps verify(k-1); "
+                                       f"select/verify {args.ctas} CTAs/SM" if args.pipeline else "serial")},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
@@ -384,6 +426,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-tokens", type=int, default=8192)
     ap.add_argument("--no-spot-check", dest="spot_check", action="store_false")
+    ap.add_argument("--no-pipeline", dest="pipeline", action="store_false")
+    ap.add_argument("--ctas", type=int, default=3, help="select/verify CTAs per SM in pipeline mode")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -106,6 +106,26 @@ int tl_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_
               uint8_t* proofs_out, void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * Launch-shape variants for pipelining a stream of batches (prove of batch k+1
+ * overlapping verify of batch k on a second stream).  ctas_per_sm caps the
+ * persistent select/verify grid (0 = occupancy maximum, 4); co_resident = 1 runs
+ * the commitment with 8 warps and a 64 KiB half inverse table so one commit CTA
+ * fits on an SM beside three select/verify CTAs.  Results are identical.
+ */
+int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
+                 int32_t H, int32_t C, int32_t K, int64_t n_chunks, int32_t* idx_out,
+                 uint16_t* bits_out, void* workspace, size_t workspace_bytes, int32_t ctas_per_sm,
+                 void* stream);
+int tl_commit_ex(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_t K,
+                 uint8_t* proofs_out, void* workspace, size_t workspace_bytes, int32_t co_resident,
+                 void* stream);
+int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
+                 int32_t H, int32_t C, int32_t K, int64_t n_chunks, const uint8_t* proofs,
+                 const tl_thresholds* thresholds_host, tl_chunk_stats* stats_out,
+                 uint8_t* chunk_accept_out, uint8_t* rollout_accept_out, void* workspace,
+                 size_t workspace_bytes, int32_t ctas_per_sm, void* stream);
+
+/*
  * VERIFY (replaces the digest compare at checks.py:209-213).
  * Re-selects top-K on the validator's hidden states, evaluates each proof at
  * the validator's indices, computes the exponent / mantissa statistics and the

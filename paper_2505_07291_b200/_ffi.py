@@ -41,6 +41,11 @@ SYMBOLS = {
                          c_vp, c_sz, c_vp]),
     "tl_select": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "tl_commit": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_sz, c_vp]),
+    "tl_select_ex": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_sz, c_i32,
+                             c_vp]),
+    "tl_commit_ex": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_sz, c_i32, c_vp]),
+    "tl_verify_ex": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_i64, c_vp,
+                             ctypes.POINTER(Thresholds), c_vp, c_vp, c_vp, c_vp, c_sz, c_i32, c_vp]),
     "tl_verify": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_i64, c_vp,
                           ctypes.POINTER(Thresholds), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "tl_round6": (c_i32, [c_vp, c_i32, c_i64, c_vp, c_vp]),

@@ -280,18 +280,22 @@ class Plan:
             raise ValueError(f"hidden must be a contiguous ({self.n_rows}, {self.H}) tensor on {self.eng.device}")
         return h
 
-    def select(self, h: torch.Tensor) -> None:
+    def _stream(self, stream) -> int:
+        return (stream if stream is not None else torch.cuda.current_stream(self.eng.device)).cuda_stream
+
+    def select(self, h: torch.Tensor, stream=None, ctas_per_sm: int = 0) -> None:
         h = self._check_hidden(h)
         e = self.eng
-        _ffi.check(e.lib.tl_select(h.data_ptr(), self.offs_dev.data_ptr(), self.n_roll, self.n_rows, self.H,
-                                   e.chunk, e.topk, self.n_chunks, self.idx.data_ptr(), self.bits.data_ptr(),
-                                   self.ws.data_ptr(), self.ws.numel(), _stream_handle(e.device)), "tl_select")
+        _ffi.check(e.lib.tl_select_ex(h.data_ptr(), self.offs_dev.data_ptr(), self.n_roll, self.n_rows, self.H,
+                                      e.chunk, e.topk, self.n_chunks, self.idx.data_ptr(), self.bits.data_ptr(),
+                                      self.ws.data_ptr(), self.ws.numel(), ctas_per_sm, self._stream(stream)),
+                   "tl_select")
 
-    def commit(self) -> None:
+    def commit(self, stream=None, co_resident: bool = False) -> None:
         e = self.eng
-        _ffi.check(e.lib.tl_commit(self.idx.data_ptr(), self.bits.data_ptr(), self.n_chunks, e.topk,
-                                   self.proofs.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
-                                   _stream_handle(e.device)), "tl_commit")
+        _ffi.check(e.lib.tl_commit_ex(self.idx.data_ptr(), self.bits.data_ptr(), self.n_chunks, e.topk,
+                                      self.proofs.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                                      1 if co_resident else 0, self._stream(stream)), "tl_commit")
 
     def prove(self, h: torch.Tensor) -> torch.Tensor:
         self.select(h)
@@ -299,17 +303,67 @@ class Plan:
         return self.proofs
 
     def verify(self, h: torch.Tensor, proofs: torch.Tensor | None = None,
-               thresholds: Thresholds = Thresholds()) -> torch.Tensor:
+               thresholds: Thresholds = Thresholds(), stream=None, ctas_per_sm: int = 0) -> torch.Tensor:
         h = self._check_hidden(h)
         e = self.eng
         pr = self.proofs if proofs is None else proofs
         th = thresholds.to_c()
-        _ffi.check(e.lib.tl_verify(h.data_ptr(), self.offs_dev.data_ptr(), self.n_roll, self.n_rows, self.H,
-                                   e.chunk, e.topk, self.n_chunks, pr.data_ptr(), ctypes.byref(th),
-                                   self.stats.data_ptr(), self.chunk_accept.data_ptr(),
-                                   self.rollout_accept.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
-                                   _stream_handle(e.device)), "tl_verify")
+        _ffi.check(e.lib.tl_verify_ex(h.data_ptr(), self.offs_dev.data_ptr(), self.n_roll, self.n_rows, self.H,
+                                      e.chunk, e.topk, self.n_chunks, pr.data_ptr(), ctypes.byref(th),
+                                      self.stats.data_ptr(), self.chunk_accept.data_ptr(),
+                                      self.rollout_accept.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                                      ctas_per_sm, self._stream(stream)), "tl_verify")
         return self.rollout_accept
+
+
+class Pipeline:
+    """Prove + verify a stream of equally-shaped batches with the commitment of batch
+    k overlapping the verification of batch k-1.
+
+    Main stream: select(k), verify(k-1), select(k+1), verify(k), ...  Side stream:
+    commit(k) after select(k).  Two buffer sets alternate; select/verify run three
+    CTAs per SM and the commitment its co-resident form, so both kernels share every
+    SM.  Results are identical to the serial ``Plan`` calls."""
+
+    def __init__(self, eng: "ToplocEngine", row_offsets, H: int, ctas_per_sm: int = 3):
+        self.plans = [Plan(eng, row_offsets, H), Plan(eng, row_offsets, H)]
+        self.eng = eng
+        self.ctas = ctas_per_sm
+        self.side = torch.cuda.Stream(eng.device)
+
+    def run(self, provers, validators, thresholds: Thresholds = Thresholds(), on_verify=None,
+            on_select=None) -> list[torch.Tensor]:
+        """provers / validators: sequences of (rows, H) device tensors.  Returns the
+        rollout-accept vectors (device uint8) per batch.  ``on_select(k)`` /
+        ``on_verify(k)`` are called around the launches (for event timing)."""
+        main = torch.cuda.current_stream(self.eng.device)
+        n = len(provers)
+        out = []
+        sel_done = [None] * n
+        com_done = [None] * n
+        for k in range(n + 1):
+            if k < n:
+                pl = self.plans[k % 2]
+                if on_select:
+                    on_select(k, "start", main)
+                pl.select(provers[k], main, self.ctas)
+                if on_select:
+                    on_select(k, "end", main)
+                sel_done[k] = torch.cuda.Event()
+                sel_done[k].record(main)
+                self.side.wait_event(sel_done[k])
+                pl.commit(self.side, co_resident=True)
+                com_done[k] = torch.cuda.Event()
+                com_done[k].record(self.side)
+            if k >= 1:
+                pl = self.plans[(k - 1) % 2]
+                main.wait_event(com_done[k - 1])
+                if on_verify:
+                    on_verify(k - 1, "start", main)
+                out.append(pl.verify(validators[k - 1], None, thresholds, main, self.ctas).clone())
+                if on_verify:
+                    on_verify(k - 1, "end", main)
+        return out
 
 
 _ENGINES: dict[tuple, ToplocEngine] = {}

@@ -52,7 +52,6 @@ constexpr int kRingStageBytes = kTileVec * 16;
 constexpr unsigned kIdxMask = 0xFFFFFFu;      // flat index field (24 bits)
 constexpr int kInvTables = 8;                 // precomputed inverse tables (first 8 primes)
 constexpr int kCommitWarps = 16;
-constexpr int kCommitThreads = kCommitWarps * 32;
 constexpr uint32_t kPMax = 65497u;
 
 // ----------------------------------------------------------------------------- helpers
@@ -819,11 +818,17 @@ __global__ void inv_table_kernel(uint16_t* __restrict__ tables) {
 
 // Inverse source for the divided differences: the CTA's shared-memory table (first
 // prime, almost every chunk), a precomputed global table (primes 2..8), or Fermat.
-enum InvMode { kInvSmem = 0, kInvGlobal = 1, kInvFermat = 2 };
+enum InvMode { kInvSmem = 0, kInvGlobal = 1, kInvFermat = 2, kInvSmemHalf = 3 };
+constexpr int kHalfTab = 32768;  // half table: inv(d) for d < 2^15, inv(d) = p - inv(p - d) above
 
 template <int MODE>
 __device__ __forceinline__ uint32_t inv_of(const uint16_t* tab, uint32_t d, const ModP& m) {
   if (MODE == kInvSmem) return tab[d];
+  if (MODE == kInvSmemHalf) {
+    const bool lo = d < (uint32_t)kHalfTab;
+    const uint32_t t = tab[lo ? d : m.p - d];
+    return lo ? t : m.p - t;
+  }
   if (MODE == kInvGlobal) return __ldg(tab + d);
   return m.pow(d, m.p - 2);
 }
@@ -895,17 +900,21 @@ __device__ __forceinline__ void interpolate_warp(const uint32_t (&x)[4], uint32_
 }
 
 // One warp per chunk: modulus search, GF(p) interpolation, 258-byte serialisation.
-__global__ void __launch_bounds__(kCommitThreads, 1)
+// WARPS x 32 threads, one CTA per SM.  HALF = 64 KiB half inverse table and <= 64
+// registers, so the CTA fits on an SM beside three select/verify CTAs (overlap mode).
+template <int WARPS, bool HALF>
+__global__ void __launch_bounds__(WARPS * 32, HALF ? 4 : 1)
 commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits, int64_t n_chunks,
               int K, const uint16_t* __restrict__ inv_tables, uint8_t* __restrict__ proofs) {
+  constexpr int kTabEntries = HALF ? kHalfTab : 65536;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint16_t* inv0 = reinterpret_cast<uint16_t*>(smem_raw);                  // 65536 x u16
-  uint32_t* xs_all = reinterpret_cast<uint32_t*>(smem_raw + 131072);     // [warps][128]
-  uint32_t* cs_all = xs_all + kCommitWarps * 128;                        // [warps][128]
+  uint16_t* inv0 = reinterpret_cast<uint16_t*>(smem_raw);
+  uint32_t* xs_all = reinterpret_cast<uint32_t*>(smem_raw + kTabEntries * 2);  // [warps][128]
+  uint32_t* cs_all = xs_all + WARPS * 128;                                     // [warps][128]
   {
     const uint4* src = reinterpret_cast<const uint4*>(inv_tables);
     uint4* dst = reinterpret_cast<uint4*>(inv0);
-    for (int i = threadIdx.x; i < 65536 * 2 / 16; i += kCommitThreads) dst[i] = src[i];
+    for (int i = threadIdx.x; i < kTabEntries * 2 / 16; i += WARPS * 32) dst[i] = src[i];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -913,8 +922,7 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
   uint32_t* cs = cs_all + warp * 128;
   const int PB = 2 + 2 * K;
 
-  for (int64_t j = (int64_t)blockIdx.x * kCommitWarps + warp; j < n_chunks;
-       j += (int64_t)gridDim.x * kCommitWarps) {
+  for (int64_t j = (int64_t)blockIdx.x * WARPS + warp; j < n_chunks; j += (int64_t)gridDim.x * WARPS) {
     uint32_t raw[4], yb[4];
     int kk = 0;
     uint32_t maxidx = 0;
@@ -973,7 +981,7 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
       xs[i] = x[r];
     }
     __syncwarp();
-    if (pi == 0) interpolate_warp<kInvSmem>(x, c, poly, xs, cs, kk, m, inv0, lane);
+    if (pi == 0) interpolate_warp<HALF ? kInvSmemHalf : kInvSmem>(x, c, poly, xs, cs, kk, m, inv0, lane);
     else if (pi < kInvTables)
       interpolate_warp<kInvGlobal>(x, c, poly, xs, cs, kk, m, inv_tables + (size_t)pi * 65536u, lane);
     else interpolate_warp<kInvFermat>(x, c, poly, xs, cs, kk, m, nullptr, lane);
@@ -1235,16 +1243,38 @@ int sm_count() {
   return n;
 }
 
-int sel_grid(int64_t n_chunks, const void* kernel) {
+int sel_grid(int64_t n_chunks, const void* kernel, int ctas_per_sm = 0) {
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSelBlockThreads, kSelSmem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
+  if (ctas_per_sm > 0 && ctas_per_sm < per_sm) per_sm = ctas_per_sm;
   const int64_t g = (int64_t)sm_count() * per_sm;
   return (int)(n_chunks < g ? (n_chunks > 0 ? n_chunks : 1) : g);
 }
 
 int launch_status() { return cudaGetLastError() == cudaSuccess ? TL_OK : TL_ECUDA; }
+
+template <int WARPS, bool HALF>
+int launch_commit_t(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, const uint16_t* tables,
+                    uint8_t* proofs, cudaStream_t st) {
+  const size_t smem = (size_t)(HALF ? kHalfTab : 65536) * 2 + 2 * WARPS * 128 * 4;
+  if (cudaFuncSetAttribute(commit_kernel<WARPS, HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return TL_ECUDA;
+  int grid = sm_count();
+  if ((int64_t)grid * WARPS > n_chunks) grid = (int)((n_chunks + WARPS - 1) / WARPS);
+  commit_kernel<WARPS, HALF><<<grid, WARPS * 32, smem, st>>>(idx, bits, n_chunks, K, tables, proofs);
+  return launch_status();
+}
+
+// co_resident = 0: 16 warps, full 128 KiB table (fastest alone); 1: 8 warps, 64 KiB
+// half table, <= 64 registers -- fits beside three select/verify CTAs per SM.
+int launch_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, const uint16_t* tables,
+                  uint8_t* proofs, int co_resident, cudaStream_t st) {
+  return co_resident ? launch_commit_t<8, true>(idx, bits, n_chunks, K, tables, proofs, st)
+                     : launch_commit_t<kCommitWarps, false>(idx, bits, n_chunks, K, tables, proofs, st);
+}
 
 }  // namespace
 
@@ -1282,6 +1312,14 @@ size_t tl_workspace_bytes(int32_t n_roll, int64_t n_chunks, int32_t K) {
 int tl_select(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
               int32_t H, int32_t C, int32_t K, int64_t n_chunks, int32_t* idx_out,
               uint16_t* bits_out, void* workspace, size_t workspace_bytes, void* stream) {
+  return tl_select_ex(hidden, row_off, n_roll, n_rows, H, C, K, n_chunks, idx_out, bits_out, workspace,
+                      workspace_bytes, 0, stream);
+}
+
+int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
+                 int32_t H, int32_t C, int32_t K, int64_t n_chunks, int32_t* idx_out,
+                 uint16_t* bits_out, void* workspace, size_t workspace_bytes, int32_t ctas_per_sm,
+                 void* stream) {
   int rc = check_shape(n_roll, n_rows, H, C, K, n_chunks);
   if (rc) return rc;
   if (n_chunks == 0 || n_roll == 0) return TL_OK;
@@ -1296,7 +1334,8 @@ int tl_select(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, in
   if (cudaFuncSetAttribute(prove_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
       cudaSuccess)
     return TL_ECUDA;
-  prove_select_kernel<<<sel_grid(n_chunks, (const void*)prove_select_kernel), kSelBlockThreads, kSelSmem, st>>>(
+  prove_select_kernel<<<sel_grid(n_chunks, (const void*)prove_select_kernel, ctas_per_sm), kSelBlockThreads,
+                        kSelSmem, st>>>(
       a, idx_out, bits_out);
   return launch_status();
 }
@@ -1313,13 +1352,22 @@ int tl_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_
   uint16_t* tables = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(workspace) + L.tables);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   inv_table_kernel<<<dim3(64, kInvTables), 256, 0, st>>>(tables);
-  const size_t smem = 131072 + 2 * kCommitWarps * 128 * 4;
-  if (cudaFuncSetAttribute(commit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return TL_ECUDA;
-  int grid = sm_count();
-  if ((int64_t)grid * kCommitWarps > n_chunks) grid = (int)((n_chunks + kCommitWarps - 1) / kCommitWarps);
-  commit_kernel<<<grid, kCommitThreads, smem, st>>>(idx, bits, n_chunks, K, tables, proofs_out);
-  return launch_status();
+  return launch_commit(idx, bits, n_chunks, K, tables, proofs_out, 0, st);
+}
+
+int tl_commit_ex(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_t K, uint8_t* proofs_out,
+                 void* workspace, size_t workspace_bytes, int32_t co_resident, void* stream) {
+  if (n_chunks < 0 || K < 1) return TL_EINVAL;
+  if (K > TL_MAX_K) return TL_EUNSUPPORTED;
+  if (n_chunks == 0) return TL_OK;
+  if (!idx || !bits || !proofs_out || !workspace) return TL_EINVAL;
+  const WsLayout L = ws_layout(0, n_chunks, K);
+  if (workspace_bytes < L.tables + (size_t)kInvTables * 65536 * 2 || (reinterpret_cast<uintptr_t>(workspace) & 255))
+    return TL_EWORKSPACE;
+  uint16_t* tables = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(workspace) + L.tables);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  inv_table_kernel<<<dim3(64, kInvTables), 256, 0, st>>>(tables);
+  return launch_commit(idx, bits, n_chunks, K, tables, proofs_out, co_resident, st);
 }
 
 int tl_prove(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
@@ -1345,6 +1393,15 @@ int tl_verify(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, in
               const tl_thresholds* thresholds_host, tl_chunk_stats* stats_out,
               uint8_t* chunk_accept_out, uint8_t* rollout_accept_out, void* workspace,
               size_t workspace_bytes, void* stream) {
+  return tl_verify_ex(hidden, row_off, n_roll, n_rows, H, C, K, n_chunks, proofs, thresholds_host, stats_out,
+                      chunk_accept_out, rollout_accept_out, workspace, workspace_bytes, 0, stream);
+}
+
+int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
+                 int32_t H, int32_t C, int32_t K, int64_t n_chunks, const uint8_t* proofs,
+                 const tl_thresholds* thresholds_host, tl_chunk_stats* stats_out,
+                 uint8_t* chunk_accept_out, uint8_t* rollout_accept_out, void* workspace,
+                 size_t workspace_bytes, int32_t ctas_per_sm, void* stream) {
   int rc = check_shape(n_roll, n_rows, H, C, K, n_chunks);
   if (rc) return rc;
   if (n_roll == 0) return TL_OK;
@@ -1362,7 +1419,8 @@ int tl_verify(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, in
     if (cudaFuncSetAttribute(verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
         cudaSuccess)
       return TL_ECUDA;
-    verify_kernel<<<sel_grid(n_chunks, (const void*)verify_kernel), kSelBlockThreads, kSelSmem, st>>>(
+    verify_kernel<<<sel_grid(n_chunks, (const void*)verify_kernel, ctas_per_sm), kSelBlockThreads, kSelSmem,
+                    st>>>(
         a, proofs, *thresholds_host, stats_out, accept);
   }
   if (rollout_accept_out)

@@ -254,3 +254,27 @@ def test_toploc_on_reference_forge_corpus():
             vb, ost, over = check_verify_against_oracle(val, offs, flat_proofs(pb), th)
             if m["kind"] == "honest":
                 assert over == [True]
+
+
+def test_pipeline_matches_serial():
+    """The two-stream pipelined schedule (commit(k) overlapping verify(k-1), 3 CTAs/SM,
+    co-resident half-table commitment) gives exactly the serial results."""
+    H, offs = 2048, [0, 160, 256, 320]
+    n = 5
+    prv = [synth_bits(400 * k, 320, H, seed=k, dist=k % 2) for k in range(n)]
+    val = [synth_bits(400 * k, 320, H, seed=k, dist=k % 2, jitter_thr=3277 * (k % 3), jitter_seed=9)
+           for k in range(n)]
+    val[3] = synth_bits(0, 320, H, seed=77)   # a wrong model in batch 3
+    dp = [torch.from_numpy(b.view(np.int16)).cuda() for b in prv]
+    dv = [torch.from_numpy(b.view(np.int16)).cuda() for b in val]
+    eng = api.engine()
+    pipe = api.Pipeline(eng, offs, H)
+    outs = pipe.run(dp, dv)
+    torch.cuda.synchronize()
+    for k in range(n):
+        pb = eng.prove(dp[k], offs)
+        vb = eng.verify(dv[k], offs, pb)
+        assert outs[k].cpu().tolist() == vb.rollout_accept.cpu().tolist(), k
+        assert pb.to_bytes() == TO.build_proofs(prv[k], offs)
+    assert torch.equal(pipe.plans[(n - 1) % 2].proofs, eng.prove(dp[n - 1], offs).proofs)
+    assert outs[3].cpu().tolist() == [0, 0, 0]
