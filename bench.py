@@ -426,7 +426,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-tokens", type=int, default=8192)
     ap.add_argument("--no-spot-check", dest="spot_check", action="store_false")
-    ap.add_argument("--no-pipeline", dest="pipeline", action="store_false")
+    ap.add_argument("--pipeline", dest="pipeline", action="store_true")
     ap.add_argument("--ctas", type=int, default=3, help="select/verify CTAs per SM in pipeline mode")
     args = ap.parse_args()
     if args.warmup < 3:
