@@ -1013,17 +1013,22 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
   const int tid = threadIdx.x;
   const int K = a.K;
   const int PB = 2 + 2 * K;
+  static_assert(kSelThreads > TL_MAX_K, "one thread per proof word");
   for (int64_t j = blockIdx.x; j < a.n_chunks; j += gridDim.x) {
     const ChunkGeo g = chunk_geo(a, j);
     const int kk = min(K, g.n);
+    // issue this chunk's proof loads (u16 t = p or c_{t-1}) before streaming, so
+    // their latency hides behind the chunk instead of the tail
+    const uint16_t* pw = reinterpret_cast<const uint16_t*>(proofs + j * PB);
+    const uint32_t pword = tid <= K ? (uint32_t)__ldg(pw + tid) : 0u;
     select_chunk(g, kk, s, src);
 
-    const uint8_t* pr = proofs + j * PB;
     if (tid == 0) {
-      s.p = ((unsigned)pr[0] << 8) | pr[1];
+      s.p = ((pword & 0xFFu) << 8) | (pword >> 8);
       s.mism = 0; s.nmatch = 0; s.msum = 0;
+    } else if (tid <= K) {
+      s.coef[tid - 1] = (uint16_t)(((pword & 0xFFu) << 8) | (pword >> 8));
     }
-    for (int i = tid; i < K; i += kSelThreads) s.coef[i] = (uint16_t)(((unsigned)pr[2 + 2 * i] << 8) | pr[3 + 2 * i]);
     if (tid < 128) s.mhist[tid] = 0;
     csync();
     const unsigned p = s.p;
