@@ -54,7 +54,9 @@ def chain_digests(rounded: np.ndarray, k: int) -> list[bytes]:
     out, prev = [], ZERO_DIGEST
     for start in range(0, max(rows, 1), k):
         stop = min(start + k, rows)
-        prev = hashlib.sha256(prev + bytes(buf[start * row_bytes:stop * row_bytes])).digest()
+        h = hashlib.sha256(prev)
+        h.update(buf[start * row_bytes:stop * row_bytes])   # zero-copy; hashlib drops the GIL
+        prev = h.digest()
         out.append(prev)
     return out
 
@@ -72,3 +74,102 @@ def build_commitments(hidden, k: int = 32) -> list[bytes]:
         raise ValueError("hidden must have at least one dimension")
     rounded = round6_device(hidden).cpu().numpy().reshape(shape)
     return chain_digests(rounded, k)
+
+
+_STAGING: dict = {}
+
+
+def _staging(dev, elems: int):
+    """Double-buffered device + pinned host float64 staging, reused across calls
+    (pinning gigabytes per call would dominate)."""
+    key = dev.index
+    cur = _STAGING.get(key)
+    if cur is None or cur[0][0].numel() < elems:
+        cur = ([torch.empty(elems, dtype=torch.float64, device=dev) for _ in range(2)],
+               [torch.empty(elems, dtype=torch.float64).pin_memory() for _ in range(2)])
+        _STAGING[key] = cur
+    return cur
+
+
+def build_commitments_batch(hidden, row_offsets, k: int = 32, threads: int | None = None,
+                            group_rows: int = 65536) -> list[list[bytes]]:
+    """Exact-mode commitments for many rollouts at once (the validator's batch form).
+
+    ``hidden`` is a (sum T, H) tensor (device or host; bf16 / f16 / f32 / f64) and
+    ``row_offsets`` delimits rollouts.  Row groups are rounded on the GPU
+    (``tl_round6``), copied to pinned host buffers on a side stream (double
+    buffered) and hashed by a thread pool -- hashlib releases the GIL, so the
+    serial-per-rollout SHA-256 chains of different rollouts run on all host cores
+    while the next group is rounded and copied.  Byte-identical to
+    ``build_commitments`` per rollout (rollout.py:51-68)."""
+    import concurrent.futures as cf
+    import os
+
+    if k < 1:
+        raise ValueError("interval must be >= 1")
+    if not torch.cuda.is_available():
+        raise RuntimeError("exact mode needs a CUDA device (no CPU fallback)")
+    t = hidden if isinstance(hidden, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(hidden))
+    if t.dim() != 2:
+        raise ValueError("hidden must be (rows, H)")
+    if t.dtype not in _DTYPE_CODE:
+        t = t.to(torch.float64)
+    offs = np.asarray(row_offsets, dtype=np.int64)
+    n_rows, H = t.shape
+    if offs[0] != 0 or offs[-1] != n_rows or np.any(np.diff(offs) < 0):
+        raise ValueError("row_offsets must start at 0, be non-decreasing and end at n_rows")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lib = _ffi.load()
+    side = torch.cuda.Stream(dev)
+    R = len(offs) - 1
+    # groups of whole rollouts, ~group_rows rows each
+    groups, start = [], 0
+    while start < R:
+        end = start + 1
+        while end < R and offs[end + 1] - offs[start] <= group_rows:
+            end += 1
+        groups.append((start, end))
+        start = end
+    max_rows = max((int(offs[e] - offs[b]) for b, e in groups), default=0)
+    dbuf, hbuf = _staging(dev, max(max_rows, 1) * H)
+    dbuf = [d[:max(max_rows, 1) * H].view(max(max_rows, 1), H) for d in dbuf]
+    hbuf = [h[:max(max_rows, 1) * H].view(max(max_rows, 1), H) for h in hbuf]
+    done = [torch.cuda.Event() for _ in range(2)]
+    out: list = [None] * R
+    pool = cf.ThreadPoolExecutor(max_workers=threads or os.cpu_count() or 1)
+    pending: list = [[], []]
+
+    def hash_rollout(r, view):
+        out[r] = chain_digests(view, k)
+
+    try:
+        for gi, (b, e) in enumerate(groups):
+            slot = gi & 1
+            for f in pending[slot]:      # host buffer free again?
+                f.result()
+            pending[slot] = []
+            r0, r1 = int(offs[b]), int(offs[e])
+            src = t[r0:r1].to(dev, non_blocking=True).contiguous()
+            rows = r1 - r0
+            if rows:
+                rc = lib.tl_round6(src.data_ptr(), _DTYPE_CODE[src.dtype], src.numel(), dbuf[slot].data_ptr(),
+                                   torch.cuda.current_stream(dev).cuda_stream)
+                _ffi.check(rc, "tl_round6")
+            ready = torch.cuda.Event()
+            ready.record(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                side.wait_event(ready)
+                if rows:
+                    hbuf[slot][:rows].copy_(dbuf[slot][:rows], non_blocking=True)
+                done[slot].record(side)
+            done[slot].synchronize()
+            host = hbuf[slot].numpy()
+            for r in range(b, e):
+                a0, a1 = int(offs[r] - r0), int(offs[r + 1] - r0)
+                pending[slot].append(pool.submit(hash_rollout, r, host[a0:a1]))
+        for slot in (0, 1):
+            for f in pending[slot]:
+                f.result()
+    finally:
+        pool.shutdown(wait=True)
+    return out

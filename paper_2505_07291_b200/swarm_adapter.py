@@ -32,6 +32,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+TOPLOC_CHUNK = 32
 _SITES = ("swarm.worker.rollout", "swarm.worker", "swarm.validator.checks", "swarm.validator.adversaries")
 _saved: dict = {}
 _claimed: contextvars.ContextVar = contextvars.ContextVar("toploc_claimed", default=None)
@@ -117,13 +118,19 @@ def install(mode: str = "exact", thresholds=None, backend=None) -> None:
     orig_validate = _saved[("swarm.validator.checks", "validate_file")]
 
     def validate_file(data, ctx, expected_identity=None):
-        from swarm.validator.checks import _commit_sample
+        from swarm.validator.checks import Verdict, _commit_sample
         from swarm.worker.files import RolloutSchemaError, parse_rollout_file
         try:
             f = parse_rollout_file(data)
             queue = [list(f.records[i].commitments) for i in sorted(_commit_sample(f, ctx))]
         except (RolloutSchemaError, Exception):
-            queue = []
+            f, queue = None, []
+        if f is not None and f.commit_interval != TOPLOC_CHUNK:
+            # TOPLOC proofs are defined over 32-token chunks; the reference trusts the
+            # header's interval (checks.py:211), TOPLOC mode enforces it
+            return Verdict(file_id=f.file_id, result="reject", failed_check="schema",
+                           details=f"commit_interval {f.commit_interval} != {TOPLOC_CHUNK}",
+                           node_address=f.node_address, step=f.step)
         token = _claimed.set(queue)
         try:
             return orig_validate(data, ctx, expected_identity)

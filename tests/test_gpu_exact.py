@@ -64,3 +64,19 @@ def test_gpu_exact_on_reference_forge_corpus():
 def test_gpu_exact_errors():
     with pytest.raises(ValueError, match="interval"):
         api.build_commitments(np.ones((2, 2)), k=0)
+
+
+def test_gpu_exact_batch_matches_reference_per_rollout():
+    rng = np.random.default_rng(4)
+    lens = [70, 0, 33, 129, 5]
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    h = rng.normal(size=(int(offs[-1]), 24))
+    from paper_2505_07291_b200.exact import build_commitments_batch
+    from oracle import exact_oracle as EO
+    got = build_commitments_batch(torch.from_numpy(h).cuda(), offs, 32, group_rows=100)
+    want = [EO.build_commitments(h[offs[r]:offs[r + 1]], 32) for r in range(len(lens))]
+    assert got == want
+    hb = torch.from_numpy(h.astype(np.float32)).to(torch.bfloat16)
+    got = build_commitments_batch(hb, offs, 7, group_rows=64)
+    want = [EO.build_commitments(hb.to(torch.float64).numpy()[offs[r]:offs[r + 1]], 7) for r in range(len(lens))]
+    assert got == want

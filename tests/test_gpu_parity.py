@@ -278,3 +278,17 @@ def test_pipeline_matches_serial():
         assert pb.to_bytes() == TO.build_proofs(prv[k], offs)
     assert torch.equal(pipe.plans[(n - 1) % 2].proofs, eng.prove(dp[n - 1], offs).proofs)
     assert outs[3].cpu().tolist() == [0, 0, 0]
+
+
+def test_scheduler_verify_sharded_single_rank():
+    from paper_2505_07291_b200 import scheduler
+    H, offs = 1024, [0, 100, 100, 164, 300]
+    prv = synth_bits(0, 300, H, seed=8)
+    val = prv.copy()
+    val[120:122] = synth_bits(1000, 2, H, seed=9)          # tamper rollout 2
+    eng = api.engine()
+    acc = scheduler.verify_sharded(eng, torch.from_numpy(prv.view(np.int16)).cuda(),
+                                   torch.from_numpy(val.view(np.int16)).cuda(), offs,
+                                   thresholds=api.Thresholds(0, 0.0, 0.0))
+    _, want = TO.verify_proofs(val, offs, TO.build_proofs(prv, offs), th=TO.Thresholds(0, 0.0, 0.0))
+    assert [bool(v) for v in acc.cpu().tolist()] == want == [True, True, False, True]

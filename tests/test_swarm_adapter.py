@@ -126,3 +126,18 @@ def test_toploc_mode_commitment_verdicts(adapter):
     adapter.install("toploc", thresholds=Thresholds(0, 0.0, 0.0), backend=OracleBackend())
     v = validate(wm, ctx)
     assert (v.result, v.failed_check) == ("reject", "commitment")
+
+
+def test_toploc_mode_enforces_commit_interval(adapter):
+    from swarm.worker.files import build_rollout_file, parse_rollout_file
+    forge, ctx = fixtures()
+    adapter.install("toploc", backend=OracleBackend())
+    f = parse_rollout_file(forge.honest(2, 0))
+    f.commit_interval = 16
+    for rec in f.records:
+        rec.commitments = rec.commitments + rec.commitments        # right count for k = 16 is irrelevant
+        rec.commitments = rec.commitments[:-(-len(rec.output_tokens) // 16)] if len(rec.commitments) > \
+            -(-len(rec.output_tokens) // 16) else rec.commitments + [rec.commitments[0]] * (
+                -(-len(rec.output_tokens) // 16) - len(rec.commitments))
+    v = validate(build_rollout_file(f, forge.key), ctx)
+    assert (v.result, v.failed_check) == ("reject", "schema") and "commit_interval" in v.details
