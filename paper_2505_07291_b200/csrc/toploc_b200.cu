@@ -29,10 +29,16 @@ namespace {
 #ifndef TL_RING
 #define TL_RING 0  // TMA ring select (1) or direct register-double-buffered loads (0)
 #endif
-constexpr int kSelThreads = 256;              // select CTA consumer threads (8 warps)
-constexpr int kSelU = 4;                      // 16-B vectors per thread per tile
+#ifndef TL_SEL_THREADS
+#define TL_SEL_THREADS 96
+#endif
+constexpr int kSelThreads = TL_SEL_THREADS;   // select CTA consumer threads
+#ifndef TL_SEL_U
+#define TL_SEL_U 4
+#endif
+constexpr int kSelU = TL_SEL_U;               // 16-B vectors per thread per tile
 #ifndef TL_SEL_MIN_BLOCKS
-#define TL_SEL_MIN_BLOCKS (TL_RING ? 2 : 4)
+#define TL_SEL_MIN_BLOCKS (TL_RING ? 2 : 8)
 #endif
 constexpr int kSelMinBlocks = TL_SEL_MIN_BLOCKS;  // resident select CTAs per SM
 constexpr int kTileVec = kSelThreads * kSelU; // 1024 vectors = 8192 bf16 per tile
@@ -327,7 +333,7 @@ __device__ __noinline__ unsigned long long block_kth_largest(const unsigned long
   unsigned long long prefix = 0, mask = 0;
   int kr = k;
   for (int shift = 48; shift >= 0; shift -= 8) {
-    if (threadIdx.x < 256) s.hist[threadIdx.x] = 0;
+    for (int b = threadIdx.x; b < 256; b += kSelThreads) s.hist[b] = 0;
     csync();
     for (int e = threadIdx.x; e < n; e += kSelThreads) {
       const unsigned long long v = buf[e];
@@ -1013,52 +1019,72 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
   const int tid = threadIdx.x;
   const int K = a.K;
   const int PB = 2 + 2 * K;
-  static_assert(kSelThreads > TL_MAX_K, "one thread per proof word");
+  constexpr int kPW = (TL_MAX_K + 1 + kSelThreads - 1) / kSelThreads;  // proof words per thread
   for (int64_t j = blockIdx.x; j < a.n_chunks; j += gridDim.x) {
     const ChunkGeo g = chunk_geo(a, j);
     const int kk = min(K, g.n);
     // issue this chunk's proof loads (u16 t = p or c_{t-1}) before streaming, so
     // their latency hides behind the chunk instead of the tail
     const uint16_t* pw = reinterpret_cast<const uint16_t*>(proofs + j * PB);
-    const uint32_t pword = tid <= K ? (uint32_t)__ldg(pw + tid) : 0u;
+    uint32_t pword[kPW];
+#pragma unroll
+    for (int q = 0; q < kPW; ++q) {
+      const int t = tid + q * kSelThreads;
+      pword[q] = t <= K ? (uint32_t)__ldg(pw + t) : 0u;
+    }
     select_chunk(g, kk, s, src);
 
-    if (tid == 0) {
-      s.p = ((pword & 0xFFu) << 8) | (pword >> 8);
-      s.mism = 0; s.nmatch = 0; s.msum = 0;
-    } else if (tid <= K) {
-      s.coef[tid - 1] = (uint16_t)(((pword & 0xFFu) << 8) | (pword >> 8));
+#pragma unroll
+    for (int q = 0; q < kPW; ++q) {
+      const int t = tid + q * kSelThreads;
+      const uint16_t v = (uint16_t)(((pword[q] & 0xFFu) << 8) | (pword[q] >> 8));
+      if (t == 0) s.p = v;
+      else if (t <= K) s.coef[t - 1] = v;
     }
-    if (tid < 128) s.mhist[tid] = 0;
+    if (tid == 0) { s.mism = 0; s.nmatch = 0; s.msum = 0; }
+    for (int b = tid; b < 128; b += kSelThreads) s.mhist[b] = 0;
     csync();
     const unsigned p = s.p;
     const bool bad = p < 2;
-    // Horner split over the two halves of the block: thread t < 128 evaluates
-    // c_0..c_{h-1} at point t, thread t + 128 evaluates c_h..c_{K-1} and scales by x^h
-    const int pt = tid & 127, half = (tid >> 7) & 1, h = (K + 1) >> 1;
-    const bool horner = tid < 256 && pt < kk;
-    uint32_t acc = 0, x = 0;
-    if (!bad && horner) {
-      const ModP m(p);
-      x = m.red(key_idx(s.out[pt]));
-      const int k_lo = half ? h : 0, k_hi = half ? K : h;
-      for (int k = k_hi - 1; k >= k_lo; --k) acc = m.red(acc * x + (uint32_t)s.coef[k]);
-      if (half) s.hpart[pt] = m.mul(acc, m.pow(x, (uint32_t)h));
-    }
-    csync();
-    if (!bad && horner && half == 0) {
-      const ModP m(p);
-      const unsigned long long v = s.out[pt];
-      const uint32_t claimed = m.add(acc, s.hpart[pt]);
+    auto tally = [&](uint32_t claimed, unsigned long long v, const ModP& m) {
       const uint32_t obs = m.red((uint32_t)(v & 0xFFFFu));
-      const uint32_t ce = (claimed >> 7) & 0xFFu, oe = (obs >> 7) & 0xFFu;
-      if (ce != oe) {
+      if (((claimed >> 7) & 0xFFu) != ((obs >> 7) & 0xFFu)) {
         atomicAdd(&s.mism, 1u);
       } else {
         const int d = abs((int)(claimed & 0x7Fu) - (int)(obs & 0x7Fu));
         atomicAdd(&s.mhist[d], 1u);
         atomicAdd(&s.msum, (unsigned)d);
         atomicAdd(&s.nmatch, 1u);
+      }
+    };
+    if constexpr (kSelThreads >= 2 * TL_MAX_K) {
+      // Horner split over two thread halves: thread t < 128 evaluates c_0..c_{h-1}
+      // at point t, thread t + 128 evaluates c_h..c_{K-1} and scales by x^h
+      const int pt = tid & 127, half = (tid >> 7) & 1, h = (K + 1) >> 1;
+      const bool horner = tid < 256 && pt < kk;
+      uint32_t acc = 0, x = 0;
+      if (!bad && horner) {
+        const ModP m(p);
+        x = m.red(key_idx(s.out[pt]));
+        const int k_lo = half ? h : 0, k_hi = half ? K : h;
+        for (int k = k_hi - 1; k >= k_lo; --k) acc = m.red(acc * x + (uint32_t)s.coef[k]);
+        if (half) s.hpart[pt] = m.mul(acc, m.pow(x, (uint32_t)h));
+      }
+      csync();
+      if (!bad && horner && half == 0) {
+        const ModP m(p);
+        tally(m.add(acc, s.hpart[pt]), s.out[pt], m);
+      }
+    } else {
+      // one Horner chain per point, TL_MAX_K / kSelThreads points per thread
+      if (!bad) {
+        const ModP m(p);
+        for (int pt = tid; pt < kk; pt += kSelThreads) {
+          const uint32_t x = m.red(key_idx(s.out[pt]));
+          uint32_t acc = 0;
+          for (int k = K - 1; k >= 0; --k) acc = m.red(acc * x + (uint32_t)s.coef[k]);
+          tally(acc, s.out[pt], m);
+        }
       }
     }
     csync();
