@@ -57,7 +57,10 @@ constexpr int kRingStages = TL_RING_STAGES;   // 16 KiB TMA stages per CTA
 constexpr int kRingStageBytes = kTileVec * 16;
 constexpr unsigned kIdxMask = 0xFFFFFFu;      // flat index field (24 bits)
 constexpr int kInvTables = 8;                 // precomputed inverse tables (first 8 primes)
-constexpr int kCommitWarps = 16;
+#ifndef TL_COMMIT_WARPS
+#define TL_COMMIT_WARPS 32
+#endif
+constexpr int kCommitWarps = TL_COMMIT_WARPS;
 constexpr uint32_t kPMax = 65497u;
 
 // ----------------------------------------------------------------------------- helpers
@@ -909,7 +912,7 @@ __device__ __forceinline__ void interpolate_warp(const uint32_t (&x)[4], uint32_
 // WARPS x 32 threads, one CTA per SM.  HALF = 64 KiB half inverse table and <= 64
 // registers, so the CTA fits on an SM beside three select/verify CTAs (overlap mode).
 template <int WARPS, bool HALF>
-__global__ void __launch_bounds__(WARPS * 32, HALF ? 4 : 1)
+__global__ void __launch_bounds__(WARPS * 32, HALF ? 4 : (WARPS > 16 ? 1 : 1))
 commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits, int64_t n_chunks,
               int K, const uint16_t* __restrict__ inv_tables, uint8_t* __restrict__ proofs) {
   constexpr int kTabEntries = HALF ? kHalfTab : 65536;
