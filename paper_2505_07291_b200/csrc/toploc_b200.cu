@@ -871,14 +871,14 @@ __device__ __forceinline__ void conv_steps(int i_hi, int i_lo, uint32_t (&poly)[
                                            const uint32_t* cs, const ModP& m, int lane) {
   const int src = (lane + 31) & 31;
   for (int i = i_hi; i >= i_lo; --i) {
-    const uint32_t xi = xs[i], ci = cs[i];
+    const uint32_t nxi = m.p - xs[i], ci = cs[i];  // prevk - x_i a == prevk + (p - x_i) a < 2^32
     uint32_t t[4];
 #pragma unroll
     for (int r = 0; r <= RM; ++r) t[r] = __shfl_sync(0xFFFFFFFFu, poly[r], src);
 #pragma unroll
     for (int r = 0; r <= RM; ++r) {
       const uint32_t prevk = lane ? t[r] : (r ? t[r > 0 ? r - 1 : 0] : (0u));
-      uint32_t nv = m.sub(prevk, m.mul(xi, poly[r]));
+      uint32_t nv = m.red(prevk + nxi * poly[r]);
       if (r == 0 && lane == 0) nv = m.add(nv, ci);
       poly[r] = nv;
     }
