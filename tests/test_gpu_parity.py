@@ -292,3 +292,14 @@ def test_scheduler_verify_sharded_single_rank():
                                    thresholds=api.Thresholds(0, 0.0, 0.0))
     _, want = TO.verify_proofs(val, offs, TO.build_proofs(prv, offs), th=TO.Thresholds(0, 0.0, 0.0))
     assert [bool(v) for v in acc.cpu().tolist()] == want == [True, True, False, True]
+
+
+@pytest.mark.parametrize("K,C,H,offs", [(64, 32, 640, [0, 70]), (1, 32, 256, [0, 40]), (128, 16, 512, [0, 50, 77]),
+                                        (17, 1, 96, [0, 9]), (128, 64, 2048, [0, 130]), (100, 8, 16384, [0, 20])])
+def test_prove_verify_other_chunk_and_topk(K, C, H, offs):
+    bits = synth_bits(0, offs[-1], H, seed=K + C, dist=1)
+    check_prove_against_oracle(bits, offs, K=K, C=C)
+    pf = [bytes(b) for b in gpu_prove(bits, offs, K, C).proofs.cpu().numpy()]
+    jit = synth_bits(0, offs[-1], H, K + C, 1, jitter_thr=6000, jitter_seed=3)
+    for th in (api.Thresholds(), api.Thresholds(0, 0.0, 0.0)):
+        check_verify_against_oracle(jit, offs, pf, th, K=K, C=C)
