@@ -46,7 +46,8 @@ constexpr int kTileElems = kTileVec * 8;
 constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kWarpCap = 256;                 // per-warp candidate buffer (2 KiB)
 static_assert(kWarpCap >= TL_MAX_K + 32, "a compaction must leave room for one full ballot");
-constexpr int kStageVec = 32 * kSelU;         // per-warp flagged-vector list (every vector of a batch)
+constexpr int kFlushAt = 4;                   // flagged vectors per exact-test round (32 lanes / 8)
+constexpr int kStageVec = 32 * kSelU + 8;     // per-warp flagged-vector queue (< kFlushAt pending + a tile)
 #ifndef TL_SPEC_HIST
 #define TL_SPEC_HIST 2  // speculation = min over the last TL_SPEC_HIST kk-th magnitudes (power of 2)
 #endif
@@ -160,6 +161,7 @@ __device__ __forceinline__ ChunkRef locate_chunk(const int64_t* __restrict__ pre
 struct SelState {
   unsigned long long wbuf[kSelWarps][kWarpCap];  // per-warp candidate keys
   int sidx[kSelWarps][kStageVec];                // per-warp flagged vector ids
+  int lst_n[kSelWarps];                          // per-warp queue lengths
 #if !TL_RING
   uint4 stage[kSelWarps][kStageVec];             // flagged vectors copied out of registers
 #endif
@@ -406,8 +408,9 @@ struct WarpScan {
   unsigned long long theta;
   int cnt;
   unsigned long long* wb;
-  int* sidx;    // flagged vector ids of the current batch
-  uint4* stg;   // TL_RING=0: flagged vectors copied out of registers
+  int* sidx;    // queued flagged vector ids
+  uint4* stg;   // TL_RING=0: queued flagged vectors copied out of registers
+  int* lst_n;   // queue length
 };
 
 __device__ __forceinline__ unsigned coarse_c2(unsigned long long theta, unsigned lo) {
@@ -436,6 +439,21 @@ __device__ __forceinline__ void test_flagged(int nflag, int a0, WarpScan& w, int
     }
     warp_append(p, key, w.wb, w.cnt, w.theta, kk, lane);
   }
+}
+
+// Test the queued flagged vectors' elements lane-parallel and empty the queue.
+template <bool STAGE>
+__device__ __forceinline__ void flush_flagged(const ChunkGeo& cg, WarpScan& w, int n, int kk, int lane) {
+  if (STAGE) {
+    const uint16_t* stg16 = reinterpret_cast<const uint16_t*>(w.stg);
+    test_flagged(n, cg.a0, w, kk, lane, [&](int e) { return (unsigned)stg16[e]; });
+  } else {
+    const uint16_t* el = cg.base + cg.a0;
+    test_flagged(n, cg.a0, w, kk, lane, [&](int e) { return (unsigned)el[8 * w.sidx[e >> 3] + (e & 7)]; });
+  }
+  __syncwarp();
+  if (lane == 0) *w.lst_n = 0;
+  __syncwarp();
 }
 
 // Chunk pass straight from HBM/L2 with a register double buffer.  Vector g of tile
@@ -470,38 +488,32 @@ __device__ __forceinline__ void pass_ldg(const ChunkGeo& cg, WarpScan& w, int kk
     for (int u = 1; u < kSelU; ++u) m = hmaxabs2(m, mu[u]);
     const bool hit = coarse_hit(m, c2);
     if (!__any_sync(0xFFFFFFFFu, hit)) continue;
-    unsigned hm = 0;
+    // queue this warp's flagged vectors (vectors past the chunk end are zero and
+    // never flagged) with one shared-memory atomic per flagged lane; test queued
+    // elements in full 32-lane rounds once >= kFlushAt vectors are pending
     if (hit) {
+      unsigned hm = 0;
 #pragma unroll
       for (int u = 0; u < kSelU; ++u)
         hm |= ((gbase + u * kSelThreads < nvec && coarse_hit(mu[u], c2)) ? 1u : 0u) << u;
-    }
-    const int c = __popc(hm);
-    int incl = c;
+      if (hm) {
+        int pos = atomicAdd(w.lst_n, __popc(hm));
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    int pos = incl - c;
-    const int tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
-#pragma unroll
-    for (int u = 0; u < kSelU; ++u) {
-      if ((hm >> u) & 1u) {
-        if (STAGE) w.stg[pos] = v[u];
-        w.sidx[pos] = gbase + u * kSelThreads;
-        ++pos;
+        for (int u = 0; u < kSelU; ++u) {
+          if ((hm >> u) & 1u) {
+            if (STAGE) w.stg[pos] = v[u];
+            w.sidx[pos] = gbase + u * kSelThreads;
+            ++pos;
+          }
+        }
       }
     }
     __syncwarp();
-    if (STAGE) {
-      const uint16_t* stg16 = reinterpret_cast<const uint16_t*>(w.stg);
-      test_flagged(tot, a0, w, kk, lane, [&](int e) { return (unsigned)stg16[e]; });
-    } else {
-      const uint16_t* el = cg.base + a0;
-      test_flagged(tot, a0, w, kk, lane, [&](int e) { return (unsigned)el[8 * w.sidx[e >> 3] + (e & 7)]; });
-    }
+    const int pending = *reinterpret_cast<volatile int*>(w.lst_n);
+    if (pending >= kFlushAt) flush_flagged<STAGE>(cg, w, pending, kk, lane);
   }
+  const int pending = *reinterpret_cast<volatile int*>(w.lst_n);
+  if (pending > 0) flush_flagged<STAGE>(cg, w, pending, kk, lane);
 }
 
 #if TL_RING
@@ -584,6 +596,7 @@ __device__ void select_chunk(const ChunkGeo& cg, int kk, SelState& s, Src& src) 
   WarpScan w;
   w.wb = s.wbuf[warp];
   w.sidx = s.sidx[warp];
+  w.lst_n = &s.lst_n[warp];
 #if TL_RING
   w.stg = nullptr;
 #else
@@ -684,6 +697,7 @@ using SelSrc = NoSrc;
 __device__ __forceinline__ bool sel_setup(uint8_t* smem, const SelArgs& a, SelState*& sp, SelSrc& src) {
   SelState& s = *reinterpret_cast<SelState*>(smem);
   sp = &s;
+  if (threadIdx.x < kSelWarps) s.lst_n[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     s.theta = 0;
     s.delta = 8;
