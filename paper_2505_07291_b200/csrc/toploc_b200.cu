@@ -48,6 +48,12 @@ constexpr int kWarpCap = 256;                 // per-warp candidate buffer (2 Ki
 static_assert(kWarpCap >= TL_MAX_K + 32, "a compaction must leave room for one full ballot");
 constexpr int kFlushAt = 4;                   // flagged vectors per exact-test round (32 lanes / 8)
 constexpr int kStageVec = 32 * kSelU + 8;     // per-warp flagged-vector queue (< kFlushAt pending + a tile)
+#ifndef TL_SPEC_LO
+#define TL_SPEC_LO 32   // adapt the margin so a chunk yields kk + [LO, HI] candidates
+#endif
+#ifndef TL_SPEC_HI
+#define TL_SPEC_HI 128
+#endif
 #ifndef TL_SPEC_HIST
 #define TL_SPEC_HIST 2  // speculation = min over the last TL_SPEC_HIST kk-th magnitudes (power of 2)
 #endif
@@ -673,8 +679,8 @@ __device__ void select_chunk(const ChunkGeo& cg, int kk, SelState& s, Src& src) 
   csync();
   if (tid == 0) {  // speculation for this CTA's next chunk
     int d = s.delta;
-    if (total > kk + 128 && d > 1) --d;
-    else if (total < kk + 32) ++d;
+    if (total > kk + TL_SPEC_HI && d > 1) --d;
+    else if (total < kk + TL_SPEC_LO) ++d;
     s.delta = d;
     s.khist[s.khead++ & (TL_SPEC_HIST - 1)] = (unsigned)(s.out[kk - 1] >> 40);
     unsigned kmag = s.khist[0];
