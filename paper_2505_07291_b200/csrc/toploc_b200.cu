@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include "../../include/toploc_b200.h"
@@ -26,44 +27,32 @@
 namespace {
 
 // ----------------------------------------------------------------------------- constants
-#ifndef TL_RING
-#define TL_RING 0  // TMA ring select (1) or direct register-double-buffered loads (0)
-#endif
 #ifndef TL_SEL_THREADS
 #define TL_SEL_THREADS 96
 #endif
-constexpr int kSelThreads = TL_SEL_THREADS;   // select CTA consumer threads
+constexpr int kSelThreads = TL_SEL_THREADS;   // select CTA threads (independent warps)
 #ifndef TL_SEL_U
 #define TL_SEL_U 4
 #endif
-constexpr int kSelU = TL_SEL_U;               // 16-B vectors per thread per tile
+constexpr int kSelU = TL_SEL_U;               // 16-B vectors per lane per warp tile
 #ifndef TL_SEL_MIN_BLOCKS
-#define TL_SEL_MIN_BLOCKS (TL_RING ? 2 : 8)
+#define TL_SEL_MIN_BLOCKS 8
 #endif
 constexpr int kSelMinBlocks = TL_SEL_MIN_BLOCKS;  // resident select CTAs per SM
-constexpr int kTileVec = kSelThreads * kSelU; // 1024 vectors = 8192 bf16 per tile
-constexpr int kTileElems = kTileVec * 8;
 constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kWarpCap = 256;                 // per-warp candidate buffer (2 KiB)
 static_assert(kWarpCap >= TL_MAX_K + 32, "a compaction must leave room for one full ballot");
 constexpr int kFlushAt = 4;                   // flagged vectors per exact-test round (32 lanes / 8)
 constexpr int kStageVec = 32 * kSelU + 8;     // per-warp flagged-vector queue (< kFlushAt pending + a tile)
 #ifndef TL_SPEC_LO
-#define TL_SPEC_LO 32   // adapt the margin so a chunk yields kk + [LO, HI] candidates
+#define TL_SPEC_LO 16   // adapt the margin so a chunk yields kk + [LO, HI] candidates
 #endif
 #ifndef TL_SPEC_HI
-#define TL_SPEC_HI 128
+#define TL_SPEC_HI 96   // < kWarpCap - TL_MAX_K: no compaction at the target
 #endif
-#ifndef TL_SPEC_HIST
-#define TL_SPEC_HIST 2  // speculation = min over the last TL_SPEC_HIST kk-th magnitudes (power of 2)
-#endif
-#ifndef TL_RING_STAGES
-#define TL_RING_STAGES 5
-#endif
-constexpr int kRingStages = TL_RING_STAGES;   // 16 KiB TMA stages per CTA
-constexpr int kRingStageBytes = kTileVec * 16;
 constexpr unsigned kIdxMask = 0xFFFFFFu;      // flat index field (24 bits)
 constexpr int kInvTables = 8;                 // precomputed inverse tables (first 8 primes)
+constexpr int kSpecSlots = 8192;              // speculation slots in the workspace (16 B each)
 #ifndef TL_COMMIT_WARPS
 #define TL_COMMIT_WARPS 32
 #endif
@@ -144,62 +133,96 @@ __device__ __forceinline__ ChunkRef locate_chunk(const int64_t* __restrict__ pre
 
 // ----------------------------------------------------------------------------- streaming select
 //
-// One CTA owns one chunk at a time (persistent over its chunks j = blockIdx.x,
-// + gridDim.x, ...).  TL_RING=1 (default): a producer warp streams the CTA's chunks
-// through a ring of kRingStages x 16 KiB shared-memory stages with TMA bulk copies
-// (cp.async.bulk + mbarrier complete_tx), running ahead across chunk boundaries so
-// ~190 KiB per SM stay in flight -- the depth a pure read needs to approach the
-// ~7.3 TB/s read ceiling measured on this part (tools/lab/bwprobe.py).  Eight
-// consumer warps filter each stage (1024 vectors, 128 per warp).  TL_RING=0: the
-// consumers load straight from HBM with a register double buffer.
+// One WARP owns one chunk at a time (persistent over chunks j = its global warp
+// id, + the total warp count, ...).  It streams the chunk's 16-byte vectors
+// (vector g of warp tile t: t*kWTileVec + u*32 + lane) through a register double
+// buffer of non-allocating loads.  Per lane and tile a bf16x2 |max| tree folds the
+// 8 U elements into one 16x2 maximum, tested with one add-and-mask against the
+// warp's threshold theta; a flagged lane queues its vectors in shared memory and
+// queued elements are tested exactly against the composite key in full 32-lane
+// rounds.  Survivors go to the warp's candidate buffer (kWarpCap keys); a full
+// buffer is compacted (bitonic sort, keep the kk largest, theta = the kk-th), so
+// the buffer always holds every element seen with key >= theta and, once theta was
+// raised by a compaction, at least kk of them: at the chunk end it contains the
+// chunk's top-kk.
 //
-// Each consumer warp keeps its own candidate buffer and threshold theta_w with
-// the invariant
-//     every element this warp has seen with key >= theta_w is in its buffer,
-// and, once theta_w was raised by a compaction, >= kk seen elements are >= theta_w.
-// The union of the warp buffers therefore contains the chunk's top-kk (an element
-// below its warp's theta_w is beaten by kk others).  No barrier while streaming;
-// the chunk ends with one consumer barrier and a warp bitonic sort.
+// There is no barrier anywhere.  The warps of a CTA are independent, so a warp's
+// chunk tail (final sort, output, verify-side evaluation) overlaps the other
+// warps' streaming and the SM keeps its loads in flight (tools/lab/chunkprobe.py:
+// a CTA-wide chunk tail of 8 us costs 6 % of the read rate, a per-warp one 1 %).
 //
-// A chunk starts from a speculative theta (the previous chunk's kk-th magnitude
-// minus an adaptive margin).  If the union ends with < kk entries the speculation
-// was too high and the chunk is re-scanned from HBM/L2 with theta = 0.
-struct SelState {
-  unsigned long long wbuf[kSelWarps][kWarpCap];  // per-warp candidate keys
-  int sidx[kSelWarps][kStageVec];                // per-warp flagged vector ids
-  int lst_n[kSelWarps];                          // per-warp queue lengths
-#if !TL_RING
-  uint4 stage[kSelWarps][kStageVec];             // flagged vectors copied out of registers
-#endif
-  unsigned long long out[TL_MAX_K];              // selected keys, rank order
-  unsigned long long theta;                      // chunk-start threshold (speculation)
-  unsigned khist[TL_SPEC_HIST];                  // last kk-th magnitudes (speculation history)
-  int khead;
-  int retry;                                     // re-scans of the current chunk
-  int wcnt[kSelWarps];
-  unsigned hist[256];
-  int delta;                                     // speculation margin, magnitude units
-  int digit;
-  int kr;
-  int n_out;
-  // verify-side scratch
-  unsigned p;
-  unsigned mism, nmatch, msum;
-  unsigned mhist[128];
-  uint32_t hpart[TL_MAX_K];
-  uint16_t coef[TL_MAX_K];
-};
-constexpr size_t kSelStateBytes = (sizeof(SelState) + 127) & ~(size_t)127;
-#if TL_RING
-constexpr int kSelBlockThreads = kSelThreads + 32;  // + producer warp
-constexpr size_t kSelSmem = kSelStateBytes + (size_t)kRingStages * kRingStageBytes + 2 * kRingStages * 8;
-#else
-constexpr int kSelBlockThreads = kSelThreads;
-constexpr size_t kSelSmem = kSelStateBytes;
-#endif
+// A chunk starts from a speculative theta (min of the warp's last two kk-th
+// magnitudes minus an adaptive margin).  If the buffer ends with < kk keys the
+// speculation excluded part of the top-kk and the chunk is re-scanned with a lower
+// threshold: 64, then 256 magnitude steps lower, then 0 (exact).
+constexpr int kWTileVec = 32 * kSelU;  // 16-B vectors per warp tile
+constexpr int kWTileElems = kWTileVec * 8;
 
-// Barrier over the consumer threads only (the producer warp never joins).
-__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(kSelThreads) : "memory"); }
+struct WarpSlot {
+  unsigned long long wbuf[kWarpCap];  // candidate keys; the sorted top-kk at chunk end
+  int sidx[kStageVec];                // queued flagged vector ids
+  uint4 stage[kStageVec];             // queued flagged vectors
+  uint16_t coef[TL_MAX_K];            // verify: the claimed coefficients
+  unsigned mhist[128];                // verify: |mantissa diff| histogram
+  int lst_n;                          // queue length
+};
+static_assert(offsetof(WarpSlot, stage) % 16 == 0 && offsetof(WarpSlot, coef) % 16 == 0, "slot alignment");
+struct SelState {
+  WarpSlot w[kSelWarps];
+};
+constexpr int kSelBlockThreads = kSelThreads;
+constexpr size_t kSelSmem = (sizeof(SelState) + 127) & ~(size_t)127;
+
+// Warp-uniform speculation state, carried in registers from chunk to chunk and,
+// through the workspace, from launch to launch (slot = global warp id mod
+// kSpecSlots; a slot that does not hold a valid state starts from theta = 0).
+// It only steers speed: any theta gives the exact top-kk.
+struct Spec {
+  unsigned long long theta;  // next chunk's starting threshold
+  unsigned k0, k1;           // the last two kk-th magnitudes
+  int delta;                 // margin below them, magnitude units
+};
+constexpr unsigned kSpecMagic = 0x53504543u;
+__device__ __forceinline__ void spec_arm(Spec& sp) {
+  const unsigned kmag = min(sp.k0, sp.k1);
+  sp.theta = kmag > (unsigned)sp.delta ? ((unsigned long long)(kmag - (unsigned)sp.delta) << 40) : 0ull;
+}
+__device__ __forceinline__ Spec spec_load(const uint4* slots, int64_t gw) {
+  const uint4 v = slots[gw % kSpecSlots];
+  Spec sp{0ull, 0x7FFFu, 0x7FFFu, 8};
+  if (v.w == kSpecMagic && v.x <= 0x7FFFu && v.y <= 0x7FFFu && v.z >= 1u && v.z <= 0x4000u) {
+    sp.k0 = v.x;
+    sp.k1 = v.y;
+    sp.delta = (int)v.z;
+    spec_arm(sp);
+  }
+  return sp;
+}
+__device__ __forceinline__ void spec_store(uint4* slots, int64_t gw, const Spec& sp, int lane) {
+  if (lane == 0 && sp.k1 <= 0x7FFFu)
+    slots[gw % kSpecSlots] = make_uint4(sp.k0, sp.k1, (unsigned)sp.delta, kSpecMagic);
+}
+
+#if TL_PHASE_PROF
+// Lab instrumentation (-DTL_PHASE_PROF=1): clock64 time per chunk phase summed over
+// warps (0 geo, 1 pass, 2 re-scans, 3 sort + speculation, 4 output / verify tail)
+// and counters (5 chunks, 6 candidates, 7 re-scanned chunks), 8 theta = 0 passes;
+// read by tl_phase_prof.
+__device__ unsigned long long g_prof[16];
+#define PROF_DECL unsigned long long prof_[16] = {}; long long prof_last_ = clock64()
+#define PROF_MARK(ph) do { const long long t_ = clock64(); prof_[ph] += t_ - prof_last_; prof_last_ = t_; } while (0)
+#define PROF_COUNT(i, v) (prof_[i] += (v))
+#define PROF_FLUSH() do { if ((threadIdx.x & 31) == 0) for (int q_ = 0; q_ < 16; ++q_) atomicAdd(&g_prof[q_], prof_[q_]); } while (0)
+#define PROF_ARG , unsigned long long (&prof_)[16], long long& prof_last_
+#define PROF_PASS , prof_, prof_last_
+#else
+#define PROF_DECL do {} while (0)
+#define PROF_MARK(ph) do {} while (0)
+#define PROF_COUNT(i, v) do {} while (0)
+#define PROF_FLUSH() do {} while (0)
+#define PROF_ARG
+#define PROF_PASS
+#endif
 
 __device__ __forceinline__ unsigned hmaxabs2(unsigned a, unsigned b) {
   unsigned d;  // per bf16 half: max(|a|, |b|) (sign = xor, masked off by the caller); NaN wins
@@ -215,50 +238,21 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return r;
 }
 
-// ---- TMA bulk copy + mbarrier primitives
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  } while (!ok);
-}
-
 // ---- chunk geometry
 struct ChunkGeo {
   const uint16_t* base;  // first element
   int n;                 // elements
   int a0;                // scalar head elements before the first 16-B boundary
   int nvec;              // 16-B vectors after the head
-  int nst;               // 1024-vector stages
+  int nst;               // warp tiles
 };
 struct SelArgs {
   const uint16_t* hidden;
   const int64_t* row_off;
   const int64_t* prefix;
+  uint4* spec;       // workspace: speculation state per warp slot, kept across launches
   int n_roll, H, C, K;
-  int64_t n_chunks;  // min(caller's n_chunks, prefix[n_roll])
+  int64_t n_chunks;  // caller's n_chunks (clamped to prefix[n_roll] in the kernels)
 };
 __device__ __forceinline__ ChunkGeo chunk_geo(const SelArgs& a, int64_t j) {
   const ChunkRef cr = locate_chunk(a.prefix, a.row_off, a.n_roll, j, a.C);
@@ -268,13 +262,13 @@ __device__ __forceinline__ ChunkGeo chunk_geo(const SelArgs& a, int64_t j) {
   const uintptr_t addr = reinterpret_cast<uintptr_t>(g.base);
   g.a0 = min(g.n, (int)(((16u - (unsigned)(addr & 15u)) & 15u) >> 1));
   g.nvec = (g.n - g.a0) >> 3;
-  g.nst = (g.nvec + kTileVec - 1) / kTileVec;
+  g.nst = (g.nvec + kWTileVec - 1) / kWTileVec;
   return g;
 }
 
 // Warp bitonic sort, descending, of NPER*32 keys held as a[r] at position r*32+lane.
-template <int NPER>
-__device__ __forceinline__ void warp_bitonic_desc(unsigned long long (&a)[NPER], int lane) {
+template <typename T, int NPER>
+__device__ __forceinline__ void warp_bitonic_desc(T (&a)[NPER], int lane) {
   constexpr int N = NPER * 32;
 #pragma unroll
   for (int k = 2; k <= N; k <<= 1) {
@@ -286,8 +280,8 @@ __device__ __forceinline__ void warp_bitonic_desc(unsigned long long (&a)[NPER],
         for (int r = 0; r < NPER; ++r) {
           if ((r & rj) == 0) {
             const bool desc = (((r * 32 + lane) & k) == 0);
-            const unsigned long long x = a[r], y = a[r | rj];
-            const unsigned long long hi = x > y ? x : y, lo = x > y ? y : x;
+            const T x = a[r], y = a[r | rj];
+            const T hi = x > y ? x : y, lo = x > y ? y : x;
             a[r] = desc ? hi : lo;
             a[r | rj] = desc ? lo : hi;
           }
@@ -295,10 +289,10 @@ __device__ __forceinline__ void warp_bitonic_desc(unsigned long long (&a)[NPER],
       } else {
 #pragma unroll
         for (int r = 0; r < NPER; ++r) {
-          const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, a[r], j);
+          const T o = __shfl_xor_sync(0xFFFFFFFFu, a[r], j);
           const bool desc = (((r * 32 + lane) & k) == 0);
           const bool lower = (lane & j) == 0;
-          const unsigned long long hi = a[r] > o ? a[r] : o, lo = a[r] > o ? o : a[r];
+          const T hi = a[r] > o ? a[r] : o, lo = a[r] > o ? o : a[r];
           a[r] = (desc == lower) ? hi : lo;
         }
       }
@@ -306,18 +300,55 @@ __device__ __forceinline__ void warp_bitonic_desc(unsigned long long (&a)[NPER],
   }
 }
 
-// Buffer full: keep the warp's kk largest keys; returns theta_w = the kk-th (rare path).
-__device__ __noinline__ unsigned long long warp_compact(unsigned long long* wb, int cnt, int kk, int lane) {
-  unsigned long long a[kWarpCap / 32];
+// Rank wb[0..cnt) descending in place (chunk end and buffer compaction).  When the
+// keys' indices are < 2^19 - 1 and their magnitudes span < 2^12 above the minimum
+// `base` (the usual case), the keys are ranked as 32-bit words
+//     (mag - base) << 20 | (2^19 - 1 - idx) << 1 | sign,
+// which order like the 64-bit keys ((mag, idx) is unique, so the sign never
+// decides) at half the shuffles and compares; otherwise as 64-bit keys.
+template <int NPER>
+__device__ __forceinline__ void final_sort(unsigned long long* wb, int cnt, int lane) {
+  unsigned long long a[NPER];
+  unsigned lo = 0xFFFFu, hi = 0u, imax = 0u;
 #pragma unroll
-  for (int r = 0; r < kWarpCap / 32; ++r) {
+  for (int r = 0; r < NPER; ++r) {
     const int q = r * 32 + lane;
     a[r] = q < cnt ? wb[q] : 0ull;
+    if (q < cnt) {
+      lo = min(lo, (unsigned)(a[r] >> 40));
+      hi = max(hi, (unsigned)(a[r] >> 40));
+      imax = max(imax, key_idx(a[r]));
+    }
   }
-  warp_bitonic_desc<kWarpCap / 32>(a, lane);
+  const unsigned base = __reduce_min_sync(0xFFFFFFFFu, lo);
+  hi = __reduce_max_sync(0xFFFFFFFFu, hi);
+  imax = __reduce_max_sync(0xFFFFFFFFu, imax);
+  if (hi - base < 4096u && imax < 0x7FFFFu) {
+    uint32_t k[NPER];
 #pragma unroll
-  for (int r = 0; r < kWarpCap / 32; ++r) wb[r * 32 + lane] = a[r];
+    for (int r = 0; r < NPER; ++r) {
+      const unsigned mag = (unsigned)(a[r] >> 40);
+      k[r] = r * 32 + lane < cnt ? ((mag - base) << 20) | ((0x7FFFFu - key_idx(a[r])) << 1) |
+                                       (unsigned)((a[r] >> 15) & 1u)
+                                 : 0u;
+    }
+    warp_bitonic_desc<uint32_t, NPER>(k, lane);
+#pragma unroll
+    for (int r = 0; r < NPER; ++r)
+      wb[r * 32 + lane] = k[r] ? make_key(((k[r] & 1u) << 15) | (base + (k[r] >> 20)), 0x7FFFFu - ((k[r] >> 1) & 0x7FFFFu))
+                               : 0ull;
+  } else {
+    warp_bitonic_desc<unsigned long long, NPER>(a, lane);
+#pragma unroll
+    for (int r = 0; r < NPER; ++r) wb[r * 32 + lane] = a[r];
+  }
   __syncwarp();
+}
+
+
+// Buffer full: keep the warp's kk largest keys; returns theta = the kk-th (rare path).
+__device__ __noinline__ unsigned long long warp_compact(unsigned long long* wb, int cnt, int kk, int lane) {
+  final_sort<kWarpCap / 32>(wb, cnt, lane);
   return wb[kk - 1];
 }
 
@@ -337,86 +368,14 @@ __device__ __forceinline__ void warp_append(bool p, unsigned long long key, unsi
   __syncwarp();
 }
 
-// k-th largest of buf[0..n) by 8-bit radix select over the 56 significant bits.
-// All consumer threads call; contains barriers.  Rare path.
-__device__ __noinline__ unsigned long long block_kth_largest(const unsigned long long* buf, int n, int k,
-                                                             SelState& s) {
-  unsigned long long prefix = 0, mask = 0;
-  int kr = k;
-  for (int shift = 48; shift >= 0; shift -= 8) {
-    for (int b = threadIdx.x; b < 256; b += kSelThreads) s.hist[b] = 0;
-    csync();
-    for (int e = threadIdx.x; e < n; e += kSelThreads) {
-      const unsigned long long v = buf[e];
-      if ((v & mask) == prefix) atomicAdd(&s.hist[(unsigned)(v >> shift) & 255u], 1u);
-    }
-    csync();
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
-      unsigned c[8], sum = 0;
-#pragma unroll
-      for (int t = 0; t < 8; ++t) { c[t] = s.hist[255 - (lane * 8 + t)]; sum += c[t]; }
-      unsigned incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const unsigned excl = incl - sum;
-      if ((int)excl < kr && kr <= (int)incl) {
-        unsigned acc = excl;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          if ((int)acc < kr && kr <= (int)(acc + c[t])) {
-            s.digit = 255 - (lane * 8 + t);
-            s.kr = kr - (int)acc;
-          }
-          acc += c[t];
-        }
-      }
-    }
-    csync();
-    prefix |= (unsigned long long)s.digit << shift;
-    mask |= 0xFFull << shift;
-    kr = s.kr;
-    csync();
-  }
-  return prefix;
-}
-
-// Final ranking when the warp buffers hold more than 256 candidates (ties,
-// degenerate chunks, theta = 0 restarts): radix-select the kk-th key over all
-// buffers, collect the kk keys >= it, sort them.  All consumer threads call.
-__device__ __noinline__ void rank_many(int kk, SelState& s) {
-  unsigned long long* all = &s.wbuf[0][0];
-  for (int e = threadIdx.x; e < kSelWarps * kWarpCap; e += kSelThreads)
-    if ((e % kWarpCap) >= s.wcnt[e / kWarpCap]) all[e] = 0ull;
-  if (threadIdx.x == 0) s.n_out = 0;
-  csync();
-  const unsigned long long th = block_kth_largest(all, kSelWarps * kWarpCap, kk, s);
-  for (int e = threadIdx.x; e < kSelWarps * kWarpCap; e += kSelThreads)
-    if (all[e] >= th && all[e] != 0ull) s.out[atomicAdd(&s.n_out, 1)] = all[e];
-  csync();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    unsigned long long a[TL_MAX_K / 32];
-#pragma unroll
-    for (int r = 0; r < TL_MAX_K / 32; ++r) a[r] = (r * 32 + lane < kk) ? s.out[r * 32 + lane] : 0ull;
-    __syncwarp();
-    warp_bitonic_desc<TL_MAX_K / 32>(a, lane);
-#pragma unroll
-    for (int r = 0; r < TL_MAX_K / 32; ++r) s.out[r * 32 + lane] = a[r];
-  }
-}
-
 // Per-warp streaming state (all members warp-uniform except the pointers' targets).
 struct WarpScan {
   unsigned long long theta;
   int cnt;
   unsigned long long* wb;
-  int* sidx;    // queued flagged vector ids
-  uint4* stg;   // TL_RING=0: queued flagged vectors copied out of registers
-  int* lst_n;   // queue length
+  int* sidx;   // queued flagged vector ids
+  uint4* stg;  // queued flagged vectors (copied out of registers)
+  int* lst_n;  // queue length
 };
 
 __device__ __forceinline__ unsigned coarse_c2(unsigned long long theta, unsigned lo) {
@@ -426,66 +385,51 @@ __device__ __forceinline__ unsigned coarse_c2(unsigned long long theta, unsigned
   return ((0x8000u - tk) & 0xFFFFu) * 0x10001u;
 }
 
-// Test the elements of `nflag` flagged vectors lane-parallel and append survivors.
-// Element e of the batch is vector sidx[e >> 3], bf16 (e & 7); its bits are read
-// through `elem(e)`.
-template <typename Elem>
-__device__ __forceinline__ void test_flagged(int nflag, int a0, WarpScan& w, int kk, int lane, Elem elem) {
+// Test the elements of the n queued vectors lane-parallel, append survivors and
+// empty the queue.  Element e of the batch is vector sidx[e >> 3], bf16 (e & 7).
+__device__ __forceinline__ void flush_flagged(const ChunkGeo& cg, WarpScan& w, int n, int kk, int lane) {
+  const uint16_t* stg16 = reinterpret_cast<const uint16_t*>(w.stg);
   const unsigned tkey = (unsigned)(w.theta >> 40);
-  for (int e0 = 0; e0 < 8 * nflag; e0 += 32) {
+  for (int e0 = 0; e0 < 8 * n; e0 += 32) {
     const int e = e0 + lane;
     bool p = false;
     unsigned long long key = 0;
-    if (e < 8 * nflag) {
-      const unsigned b = elem(e);
+    if (e < 8 * n) {
+      const unsigned b = stg16[e];
       if ((b & 0x7FFFu) >= tkey) {
-        key = make_key(b, (unsigned)(a0 + 8 * w.sidx[e >> 3] + (e & 7)));
+        key = make_key(b, (unsigned)(cg.a0 + 8 * w.sidx[e >> 3] + (e & 7)));
         p = key >= w.theta;
       }
     }
     warp_append(p, key, w.wb, w.cnt, w.theta, kk, lane);
-  }
-}
-
-// Test the queued flagged vectors' elements lane-parallel and empty the queue.
-template <bool STAGE>
-__device__ __forceinline__ void flush_flagged(const ChunkGeo& cg, WarpScan& w, int n, int kk, int lane) {
-  if (STAGE) {
-    const uint16_t* stg16 = reinterpret_cast<const uint16_t*>(w.stg);
-    test_flagged(n, cg.a0, w, kk, lane, [&](int e) { return (unsigned)stg16[e]; });
-  } else {
-    const uint16_t* el = cg.base + cg.a0;
-    test_flagged(n, cg.a0, w, kk, lane, [&](int e) { return (unsigned)el[8 * w.sidx[e >> 3] + (e & 7)]; });
   }
   __syncwarp();
   if (lane == 0) *w.lst_n = 0;
   __syncwarp();
 }
 
-// Chunk pass straight from HBM/L2 with a register double buffer.  Vector g of tile
-// t: t*1024 + u*256 + warp*32 + lane.  Flagged vectors are copied to w.stg
-// (STAGE) or their elements re-read from global memory (L2-hot; the TL_RING
-// restart path, which has no staging buffer).
-template <bool STAGE>
-__device__ __forceinline__ void pass_ldg(const ChunkGeo& cg, WarpScan& w, int kk, int warp, int lane) {
+// One pass of the warp over its chunk straight from HBM with a register double
+// buffer; flagged vectors are queued with one shared-memory atomic per flagged
+// lane and tested in full 32-lane rounds once >= kFlushAt are pending.
+__device__ __forceinline__ void pass_warp(const ChunkGeo& cg, WarpScan& w, int kk, int lane) {
   const uint4* __restrict__ vb = reinterpret_cast<const uint4*>(cg.base + cg.a0);
   const int nvec = cg.nvec, a0 = cg.a0;
   uint4 vn[kSelU];
 #pragma unroll
   for (int u = 0; u < kSelU; ++u) {
-    const int g = warp * 32 + lane + u * kSelThreads;
+    const int g = lane + u * 32;
     vn[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
   }
   for (int it = 0; it < cg.nst; ++it) {
-    const int gbase = it * kTileVec + warp * 32 + lane;
+    const int gbase = it * kWTileVec + lane;
     uint4 v[kSelU];
 #pragma unroll
     for (int u = 0; u < kSelU; ++u) {
       v[u] = vn[u];
-      const int g = gbase + kTileVec + u * kSelThreads;
+      const int g = gbase + kWTileVec + u * 32;
       vn[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
     }
-    const unsigned c2 = coarse_c2(w.theta, (unsigned)(a0 + it * kTileElems));
+    const unsigned c2 = coarse_c2(w.theta, (unsigned)(a0 + it * kWTileElems));
     unsigned mu[kSelU];
 #pragma unroll
     for (int u = 0; u < kSelU; ++u) mu[u] = hmaxabs2(hmaxabs2(v[u].x, v[u].y), hmaxabs2(v[u].z, v[u].w));
@@ -494,21 +438,19 @@ __device__ __forceinline__ void pass_ldg(const ChunkGeo& cg, WarpScan& w, int kk
     for (int u = 1; u < kSelU; ++u) m = hmaxabs2(m, mu[u]);
     const bool hit = coarse_hit(m, c2);
     if (!__any_sync(0xFFFFFFFFu, hit)) continue;
-    // queue this warp's flagged vectors (vectors past the chunk end are zero and
-    // never flagged) with one shared-memory atomic per flagged lane; test queued
-    // elements in full 32-lane rounds once >= kFlushAt vectors are pending
+    // vectors past the chunk end are zero and never flagged
     if (hit) {
       unsigned hm = 0;
 #pragma unroll
       for (int u = 0; u < kSelU; ++u)
-        hm |= ((gbase + u * kSelThreads < nvec && coarse_hit(mu[u], c2)) ? 1u : 0u) << u;
+        hm |= ((gbase + u * 32 < nvec && coarse_hit(mu[u], c2)) ? 1u : 0u) << u;
       if (hm) {
         int pos = atomicAdd(w.lst_n, __popc(hm));
 #pragma unroll
         for (int u = 0; u < kSelU; ++u) {
           if ((hm >> u) & 1u) {
-            if (STAGE) w.stg[pos] = v[u];
-            w.sidx[pos] = gbase + u * kSelThreads;
+            w.stg[pos] = v[u];
+            w.sidx[pos] = gbase + u * 32;
             ++pos;
           }
         }
@@ -516,106 +458,28 @@ __device__ __forceinline__ void pass_ldg(const ChunkGeo& cg, WarpScan& w, int kk
     }
     __syncwarp();
     const int pending = *reinterpret_cast<volatile int*>(w.lst_n);
-    if (pending >= kFlushAt) flush_flagged<STAGE>(cg, w, pending, kk, lane);
+    if (pending >= kFlushAt) flush_flagged(cg, w, pending, kk, lane);
   }
   const int pending = *reinterpret_cast<volatile int*>(w.lst_n);
-  if (pending > 0) flush_flagged<STAGE>(cg, w, pending, kk, lane);
+  if (pending > 0) flush_flagged(cg, w, pending, kk, lane);
 }
 
-#if TL_RING
-// Ring consumer: this warp's share (vectors warp*128 + u*32 + lane) of every stage
-// of the chunk, in the producer's order.  Flagged elements are read straight from
-// the stage, which is released to the producer afterwards.
-struct Ring {
-  const uint4* stages;           // [kRingStages][kTileVec]
-  unsigned long long* full;      // [kRingStages] producer -> consumers
-  unsigned long long* empty;     // [kRingStages] consumers -> producer (count = consumer warps)
-  uint32_t seq;                  // stages consumed by this warp
-};
-__device__ __forceinline__ void pass_ring(const ChunkGeo& cg, WarpScan& w, Ring& r, int kk, int warp, int lane) {
-  const int nvec = cg.nvec, a0 = cg.a0;
-  const int q0 = warp * (kTileVec / kSelWarps) + lane;
-  for (int st = 0; st < cg.nst; ++st) {
-    const uint32_t slot = r.seq % kRingStages;
-    mbar_wait(r.full + slot, (r.seq / kRingStages) & 1u);
-    const uint4* __restrict__ stage = r.stages + (size_t)slot * kTileVec;
-    const int g0 = st * kTileVec;  // vector id of stage slot 0
-    unsigned mu[kSelU];
-#pragma unroll
-    for (int u = 0; u < kSelU; ++u) {
-      const uint4 v = g0 + q0 + u * 32 < nvec ? stage[q0 + u * 32] : make_uint4(0u, 0u, 0u, 0u);
-      mu[u] = hmaxabs2(hmaxabs2(v.x, v.y), hmaxabs2(v.z, v.w));
-    }
-    unsigned m = mu[0];
-#pragma unroll
-    for (int u = 1; u < kSelU; ++u) m = hmaxabs2(m, mu[u]);
-    const unsigned c2 = coarse_c2(w.theta, (unsigned)(a0 + st * kTileElems));
-    const bool hit = coarse_hit(m, c2);
-    if (__any_sync(0xFFFFFFFFu, hit)) {
-      // u-major list of flagged stage slots (ballots only)
-      const unsigned lt = lanemask_lt();
-      int tot = 0;
-#pragma unroll
-      for (int u = 0; u < kSelU; ++u) {
-        const bool f = hit && g0 + q0 + u * 32 < nvec && coarse_hit(mu[u], c2);
-        const unsigned bal = __ballot_sync(0xFFFFFFFFu, f);
-        if (f) w.sidx[tot + __popc(bal & lt)] = q0 + u * 32;
-        tot += __popc(bal);
-      }
-      __syncwarp();
-      const uint16_t* st16 = reinterpret_cast<const uint16_t*>(stage);
-      const int a0s = a0 + 8 * g0;  // element index of stage slot 0
-      test_flagged(tot, a0s, w, kk, lane, [&](int e) { return (unsigned)st16[w.sidx[e >> 3] * 8 + (e & 7)]; });
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(r.empty + slot);
-    ++r.seq;
-  }
-}
-
-// Producer warp: stream every chunk of this CTA, stage by stage, into the ring.
-__device__ void ring_producer(const SelArgs& a, uint4* stages, unsigned long long* full,
-                              unsigned long long* empty, int lane) {
-  uint32_t seq = 0;
-  for (int64_t j = blockIdx.x; j < a.n_chunks; j += gridDim.x) {
-    const ChunkGeo g = chunk_geo(a, j);
-    const uint4* src = reinterpret_cast<const uint4*>(g.base + g.a0);
-    for (int st = 0; st < g.nst; ++st, ++seq) {
-      const uint32_t slot = seq % kRingStages;
-      if (seq >= (uint32_t)kRingStages) mbar_wait(empty + slot, ((seq / kRingStages) - 1u) & 1u);
-      if (lane == 0) {
-        const uint32_t bytes = (uint32_t)min(kTileVec, g.nvec - st * kTileVec) * 16u;
-        mbar_expect_tx(full + slot, bytes);
-        bulk_g2s(stages + (size_t)slot * kTileVec, src + (size_t)st * kTileVec, bytes, full + slot);
-      }
-      __syncwarp();
-    }
-  }
-}
-#endif
-
-// Top-kk of chunk cg -> s.out[0..kk) in rank order.  s.theta holds this chunk's
-// speculative threshold on entry.  Consumer threads only; ends with a barrier.
-template <typename Src>
-__device__ void select_chunk(const ChunkGeo& cg, int kk, SelState& s, Src& src) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// Top-kk of chunk cg -> slot.wbuf[0..kk) in rank order (descending key).
+// Warp-level; sp carries the speculation from chunk to chunk.  Returns the
+// candidate count of the final pass.
+__device__ int select_chunk(const ChunkGeo& cg, int kk, WarpSlot& slot, Spec& sp, int lane PROF_ARG) {
   WarpScan w;
-  w.wb = s.wbuf[warp];
-  w.sidx = s.sidx[warp];
-  w.lst_n = &s.lst_n[warp];
-#if TL_RING
-  w.stg = nullptr;
-#else
-  w.stg = s.stage[warp];
-#endif
+  w.wb = slot.wbuf;
+  w.sidx = slot.sidx;
+  w.stg = slot.stage;
+  w.lst_n = &slot.lst_n;
   const int tail0 = cg.a0 + (cg.nvec << 3);
-  int total;
-  bool first_pass = true;
+  unsigned long long theta0 = sp.theta;
+  int retry = 0;
   for (;;) {
-    w.theta = s.theta;
+    w.theta = theta0;
     w.cnt = 0;
-    const bool spec = w.theta != 0ull;
-    if (warp == 0) {  // scalar head / tail elements (chunks not 16-B aligned)
+    {  // scalar head / tail elements (chunks not 16-B aligned)
       bool p = false;
       unsigned long long key = 0;
       if (lane < cg.a0) {
@@ -627,115 +491,35 @@ __device__ void select_chunk(const ChunkGeo& cg, int kk, SelState& s, Src& src) 
       }
       warp_append(p, key, w.wb, w.cnt, w.theta, kk, lane);
     }
-#if TL_RING
-    if (first_pass) pass_ring(cg, w, src, kk, warp, lane);
-    else pass_ldg<false>(cg, w, kk, warp, lane);
-#else
-    pass_ldg<true>(cg, w, kk, warp, lane);
-#endif
-    first_pass = false;
-    if (lane == 0) s.wcnt[warp] = w.cnt;
-    csync();
-    total = 0;
-#pragma unroll
-    for (int q = 0; q < kSelWarps; ++q) total += s.wcnt[q];
-    if (total >= kk) break;
-    // the speculative theta excluded part of the top-kk: re-scan (L2-hot) with a
-    // lower threshold -- 64, then 256 magnitude steps lower, then 0 (exact)
-    if (!spec) __trap();  // unreachable: theta = 0 admits every element
-    csync();
-    if (tid == 0) {
-      const unsigned key = (unsigned)(s.theta >> 40);
-      const unsigned drop = s.retry == 0 ? 64u : 256u;
-      s.theta = (s.retry < 2 && key > drop) ? ((unsigned long long)(key - drop) << 40) : 0ull;
-      ++s.retry;
-      s.delta = min(s.delta + 4, 0x4000);
-    }
-    csync();
+    pass_warp(cg, w, kk, lane);
+    PROF_MARK(retry ? 2 : (theta0 ? 1 : 8));
+    if (w.cnt >= kk) break;
+    // the speculative theta excluded part of the top-kk: re-scan with a lower one
+    if (theta0 == 0ull) __trap();  // unreachable: theta = 0 admits every element
+    const unsigned key = (unsigned)(theta0 >> 40);
+    const unsigned drop = retry == 0 ? 64u : 256u;
+    theta0 = (retry < 2 && key > drop) ? ((unsigned long long)(key - drop) << 40) : 0ull;
+    PROF_COUNT(7, retry == 0);
+    ++retry;
+    sp.delta = min(sp.delta + 4, 0x4000);
   }
-
-  if (total <= 256) {
-    if (warp == 0) {
-      unsigned long long a[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int q = r * 32 + lane;
-        int run = 0, ww = 0, basew = 0;
-#pragma unroll
-        for (int t = 0; t < kSelWarps; ++t) {  // segment of q in the concatenated warp buffers
-          if (q >= run) { ww = t; basew = run; }
-          run += s.wcnt[t];
-        }
-        a[r] = q < total ? s.wbuf[ww][q - basew] : 0ull;
-      }
-      warp_bitonic_desc<8>(a, lane);
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-        if (r * 32 + lane < kk) s.out[r * 32 + lane] = a[r];
-    }
-  } else {
-    rank_many(kk, s);
-  }
-  csync();
-  if (tid == 0) {  // speculation for this CTA's next chunk
-    int d = s.delta;
-    if (total > kk + TL_SPEC_HI && d > 1) --d;
-    else if (total < kk + TL_SPEC_LO) ++d;
-    s.delta = d;
-    s.khist[s.khead++ & (TL_SPEC_HIST - 1)] = (unsigned)(s.out[kk - 1] >> 40);
-    unsigned kmag = s.khist[0];
-#pragma unroll
-    for (int q = 1; q < TL_SPEC_HIST; ++q) kmag = min(kmag, s.khist[q]);  // min of the last kk-th magnitudes
-    s.theta = kmag > (unsigned)d ? ((unsigned long long)(kmag - (unsigned)d) << 40) : 0ull;
-    s.retry = 0;
-  }
-}
-
-struct NoSrc {};
-#if TL_RING
-using SelSrc = Ring;
-#else
-using SelSrc = NoSrc;
-#endif
-
-// Carve shared memory; the producer warp (TL_RING) streams and returns false,
-// consumer threads get their ring view and return true.
-__device__ __forceinline__ bool sel_setup(uint8_t* smem, const SelArgs& a, SelState*& sp, SelSrc& src) {
-  SelState& s = *reinterpret_cast<SelState*>(smem);
-  sp = &s;
-  if (threadIdx.x < kSelWarps) s.lst_n[threadIdx.x] = 0;
-  if (threadIdx.x == 0) {
-    s.theta = 0;
-    s.delta = 8;
-    s.khead = 0;
-    s.retry = 0;
-    for (int i = 0; i < TL_SPEC_HIST; ++i) s.khist[i] = 0x7FFFu;
-  }
-#if TL_RING
-  uint4* stages = reinterpret_cast<uint4*>(smem + kSelStateBytes);
-  unsigned long long* full =
-      reinterpret_cast<unsigned long long*>(smem + kSelStateBytes + (size_t)kRingStages * kRingStageBytes);
-  unsigned long long* empty = full + kRingStages;
-  if (threadIdx.x < kRingStages) {
-    mbar_init(full + threadIdx.x, 1);
-    mbar_init(empty + threadIdx.x, kSelWarps);
-  }
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-  if (threadIdx.x >= kSelThreads) {
-    ring_producer(a, stages, full, empty, threadIdx.x & 31);
-    return false;
-  }
-  src.stages = stages;
-  src.full = full;
-  src.empty = empty;
-  src.seq = 0;
-#else
-  (void)a;
-  (void)src;
-  __syncthreads();
-#endif
-  return true;
+  const int cnt = w.cnt;
+  if (cnt <= 64) final_sort<2>(w.wb, cnt, lane);
+  else if (cnt <= 128) final_sort<4>(w.wb, cnt, lane);
+  else final_sort<8>(w.wb, cnt, lane);
+  // speculation for this warp's next chunk
+  // (theta only rises by a buffer compaction: a compacting chunk had too many candidates)
+  int d = sp.delta;
+  if ((cnt > kk + TL_SPEC_HI || w.theta != theta0) && d > 1) --d;
+  else if (cnt < kk + TL_SPEC_LO) ++d;
+  sp.delta = d;
+  sp.k0 = sp.k1;
+  sp.k1 = (unsigned)(w.wb[kk - 1] >> 40);
+  spec_arm(sp);
+  PROF_COUNT(5, 1);
+  PROF_COUNT(6, cnt);
+  PROF_MARK(3);
+  return cnt;
 }
 
 // ----------------------------------------------------------------------------- kernels
@@ -780,19 +564,24 @@ __global__ void chunk_prefix_kernel(const int64_t* __restrict__ row_off, int n_r
 __global__ void __launch_bounds__(kSelBlockThreads, kSelMinBlocks)
 prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restrict__ bits_out) {
   extern __shared__ __align__(128) uint8_t sel_smem[];
-  a.n_chunks = min(a.n_chunks, a.prefix[a.n_roll]);
-  SelState* sp;
-  SelSrc src;
-  if (!sel_setup(sel_smem, a, sp, src)) return;  // producer warp done
-  SelState& s = *sp;
+  WarpSlot& slot = reinterpret_cast<SelState*>(sel_smem)->w[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) slot.lst_n = 0;
+  __syncwarp();
+  const int64_t n_chunks = min(a.n_chunks, a.prefix[a.n_roll]);
+  const int64_t nw = (int64_t)gridDim.x * kSelWarps;
   const int K = a.K;
-  for (int64_t j = blockIdx.x; j < a.n_chunks; j += gridDim.x) {
+  const int64_t gw = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5);
+  Spec sp = spec_load(a.spec, gw);
+  PROF_DECL;
+  for (int64_t j = gw; j < n_chunks; j += nw) {
     const ChunkGeo g = chunk_geo(a, j);
     const int kk = min(K, g.n);
-    select_chunk(g, kk, s, src);
-    for (int i = threadIdx.x; i < K; i += kSelThreads) {
+    PROF_MARK(0);
+    select_chunk(g, kk, slot, sp, lane PROF_PASS);
+    for (int i = lane; i < K; i += 32) {
       if (i < kk) {
-        const unsigned long long v = s.out[i];
+        const unsigned long long v = slot.wbuf[i];
         idx_out[j * K + i] = (int32_t)key_idx(v);
         bits_out[j * K + i] = (uint16_t)(v & 0xFFFFu);
       } else {
@@ -800,8 +589,11 @@ prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restri
         bits_out[j * K + i] = 0;
       }
     }
-    csync();
+    __syncwarp();
+    PROF_MARK(4);
   }
+  spec_store(a.spec, gw, sp, lane);
+  PROF_FLUSH();
 }
 
 // Warp-wide bitonic sort (ascending over i = lane + 32 r) of 4 registers per lane.
@@ -1030,138 +822,146 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
   }
 }
 
+// Verify: the warp selects its chunk's top-kk on the validator tensor, evaluates
+// the claimed polynomial at the kk indices (Horner, four points per lane),
+// compares exponent and mantissa bits with the observed values mod p, and writes
+// the chunk statistics and verdict.
 __global__ void __launch_bounds__(kSelBlockThreads, kSelMinBlocks)
 verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
               tl_chunk_stats* __restrict__ stats_out, uint8_t* __restrict__ accept_out) {
   extern __shared__ __align__(128) uint8_t sel_smem[];
-  a.n_chunks = min(a.n_chunks, a.prefix[a.n_roll]);
-  SelState* sp;
-  SelSrc src;
-  if (!sel_setup(sel_smem, a, sp, src)) return;  // producer warp done
-  SelState& s = *sp;
-  const int tid = threadIdx.x;
+  WarpSlot& slot = reinterpret_cast<SelState*>(sel_smem)->w[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) slot.lst_n = 0;
+  __syncwarp();
+  const int64_t n_chunks = min(a.n_chunks, a.prefix[a.n_roll]);
+  const int64_t nw = (int64_t)gridDim.x * kSelWarps;
   const int K = a.K;
   const int PB = 2 + 2 * K;
-  constexpr int kPW = (TL_MAX_K + 1 + kSelThreads - 1) / kSelThreads;  // proof words per thread
-  for (int64_t j = blockIdx.x; j < a.n_chunks; j += gridDim.x) {
+  constexpr int kPW = (TL_MAX_K + 1 + 31) / 32;  // proof words per lane
+  const int64_t gw = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5);
+  Spec sp = spec_load(a.spec, gw);
+  PROF_DECL;
+  for (int64_t j = gw; j < n_chunks; j += nw) {
     const ChunkGeo g = chunk_geo(a, j);
     const int kk = min(K, g.n);
     // issue this chunk's proof loads (u16 t = p or c_{t-1}) before streaming, so
-    // their latency hides behind the chunk instead of the tail
+    // their latency hides behind the chunk
     const uint16_t* pw = reinterpret_cast<const uint16_t*>(proofs + j * PB);
     uint32_t pword[kPW];
 #pragma unroll
     for (int q = 0; q < kPW; ++q) {
-      const int t = tid + q * kSelThreads;
+      const int t = lane + 32 * q;
       pword[q] = t <= K ? (uint32_t)__ldg(pw + t) : 0u;
     }
-    select_chunk(g, kk, s, src);
+    PROF_MARK(0);
+    select_chunk(g, kk, slot, sp, lane PROF_PASS);
 
+    // claimed coefficients (big-endian u16) -> slot.coef, zero-padded to TL_MAX_K
+    unsigned p = 0;
 #pragma unroll
     for (int q = 0; q < kPW; ++q) {
-      const int t = tid + q * kSelThreads;
-      const uint16_t v = (uint16_t)(((pword[q] & 0xFFu) << 8) | (pword[q] >> 8));
-      if (t == 0) s.p = v;
-      else if (t <= K) s.coef[t - 1] = v;
+      const int t = lane + 32 * q;
+      const unsigned v = ((pword[q] & 0xFFu) << 8) | (pword[q] >> 8);
+      if (t == 0) p = v;
+      else if (t <= TL_MAX_K) slot.coef[t - 1] = (uint16_t)(t <= K ? v : 0u);
     }
-    if (tid == 0) { s.mism = 0; s.nmatch = 0; s.msum = 0; }
-    for (int b = tid; b < 128; b += kSelThreads) s.mhist[b] = 0;
-    csync();
-    const unsigned p = s.p;
+    p = __shfl_sync(0xFFFFFFFFu, p, 0);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) slot.mhist[lane + 32 * r] = 0;
+    __syncwarp();
     const bool bad = p < 2;
-    auto tally = [&](uint32_t claimed, unsigned long long v, const ModP& m) {
-      const uint32_t obs = m.red((uint32_t)(v & 0xFFFFu));
-      if (((claimed >> 7) & 0xFFu) != ((obs >> 7) & 0xFFu)) {
-        atomicAdd(&s.mism, 1u);
-      } else {
-        const int d = abs((int)(claimed & 0x7Fu) - (int)(obs & 0x7Fu));
-        atomicAdd(&s.mhist[d], 1u);
-        atomicAdd(&s.msum, (unsigned)d);
-        atomicAdd(&s.nmatch, 1u);
+    unsigned mism = 0, msum = 0, nmatch = 0;
+    if (!bad) {
+      const ModP m(p);
+      uint32_t x[4], acc[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = lane + 32 * r;
+        x[r] = i < kk ? m.red(key_idx(slot.wbuf[i])) : 0u;
+        acc[r] = 0u;
       }
-    };
-    if constexpr (kSelThreads >= 2 * TL_MAX_K) {
-      // Horner split over two thread halves: thread t < 128 evaluates c_0..c_{h-1}
-      // at point t, thread t + 128 evaluates c_h..c_{K-1} and scales by x^h
-      const int pt = tid & 127, half = (tid >> 7) & 1, h = (K + 1) >> 1;
-      const bool horner = tid < 256 && pt < kk;
-      uint32_t acc = 0, x = 0;
-      if (!bad && horner) {
-        const ModP m(p);
-        x = m.red(key_idx(s.out[pt]));
-        const int k_lo = half ? h : 0, k_hi = half ? K : h;
-        for (int k = k_hi - 1; k >= k_lo; --k) acc = m.red(acc * x + (uint32_t)s.coef[k]);
-        if (half) s.hpart[pt] = m.mul(acc, m.pow(x, (uint32_t)h));
+      const uint4* c8 = reinterpret_cast<const uint4*>(slot.coef);
+      for (int kb = (K + 7) / 8 - 1; kb >= 0; --kb) {
+        const uint4 q = c8[kb];
+        const uint32_t cw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int e = 7; e >= 0; --e) {
+          const uint32_t c = (cw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[r] = m.red(acc[r] * x[r] + c);
+        }
       }
-      csync();
-      if (!bad && horner && half == 0) {
-        const ModP m(p);
-        tally(m.add(acc, s.hpart[pt]), s.out[pt], m);
-      }
-    } else {
-      // one Horner chain per point, TL_MAX_K / kSelThreads points per thread
-      if (!bad) {
-        const ModP m(p);
-        for (int pt = tid; pt < kk; pt += kSelThreads) {
-          const uint32_t x = m.red(key_idx(s.out[pt]));
-          uint32_t acc = 0;
-          for (int k = K - 1; k >= 0; --k) acc = m.red(acc * x + (uint32_t)s.coef[k]);
-          tally(acc, s.out[pt], m);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = lane + 32 * r;
+        if (i < kk) {
+          const uint32_t obs = m.red((uint32_t)(slot.wbuf[i] & 0xFFFFu));
+          const uint32_t claimed = acc[r];
+          if (((claimed >> 7) & 0xFFu) != ((obs >> 7) & 0xFFu)) {
+            ++mism;
+          } else {
+            const unsigned d = (unsigned)abs((int)(claimed & 0x7Fu) - (int)(obs & 0x7Fu));
+            atomicAdd(&slot.mhist[d], 1u);
+            msum += d;
+            ++nmatch;
+          }
         }
       }
     }
-    csync();
-    if (tid < 32) {  // median over the 128-bin histogram of |mantissa diff|
-      const unsigned nm = s.nmatch;
-      unsigned c4[4], sum = 0;
+    mism = __reduce_add_sync(0xFFFFFFFFu, mism);
+    msum = __reduce_add_sync(0xFFFFFFFFu, msum);
+    const unsigned nm = __reduce_add_sync(0xFFFFFFFFu, nmatch);
+    __syncwarp();
+    // median over the 128-bin histogram (statistics.median: mean of the two middle values)
+    unsigned c4[4], sum = 0;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) { c4[t] = s.mhist[tid * 4 + t]; sum += c4[t]; }
-      unsigned incl = sum;
+    for (int t = 0; t < 4; ++t) { c4[t] = slot.mhist[lane * 4 + t]; sum += c4[t]; }
+    unsigned incl = sum;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (tid >= o) incl += y;
-      }
-      unsigned acc = incl - sum;
-      int v1 = -1, v2 = -1;
-      const unsigned q1 = nm ? (nm - 1) / 2 : 0, q2 = nm / 2;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    unsigned accb = incl - sum;
+    int v1 = -1, v2 = -1;
+    const unsigned q1 = nm ? (nm - 1) / 2 : 0, q2 = nm / 2;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        if (acc <= q1 && q1 < acc + c4[t]) v1 = tid * 4 + t;
-        if (acc <= q2 && q2 < acc + c4[t]) v2 = tid * 4 + t;
-        acc += c4[t];
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        v1 = max(v1, __shfl_xor_sync(0xFFFFFFFFu, v1, o));
-        v2 = max(v2, __shfl_xor_sync(0xFFFFFFFFu, v2, o));
-      }
-      if (tid == 0) {
-        tl_chunk_stats st;
-        if (bad) {
-          st.exp_mismatch = (uint32_t)kk; st.n_match = 0; st.mant_sum = 0;
+    for (int t = 0; t < 4; ++t) {
+      if (accb <= q1 && q1 < accb + c4[t]) v1 = lane * 4 + t;
+      if (accb <= q2 && q2 < accb + c4[t]) v2 = lane * 4 + t;
+      accb += c4[t];
+    }
+    v1 = __reduce_max_sync(0xFFFFFFFFu, v1);
+    v2 = __reduce_max_sync(0xFFFFFFFFu, v2);
+    if (lane == 0) {
+      tl_chunk_stats st;
+      if (bad) {
+        st.exp_mismatch = (uint32_t)kk; st.n_match = 0; st.mant_sum = 0;
+        st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
+        st.mant_median = st.mant_mean;
+        st.flags = TL_STAT_BADPROOF;
+      } else {
+        st.exp_mismatch = mism; st.n_match = nm; st.mant_sum = msum;
+        if (nm) {
+          st.mant_mean = (double)msum / (double)nm;
+          st.mant_median = ((double)v1 + (double)v2) * 0.5;
+        } else {
           st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
           st.mant_median = st.mant_mean;
-          st.flags = TL_STAT_BADPROOF;
-        } else {
-          st.exp_mismatch = s.mism; st.n_match = nm; st.mant_sum = s.msum;
-          if (nm) {
-            st.mant_mean = (double)s.msum / (double)nm;
-            st.mant_median = ((double)v1 + (double)v2) * 0.5;
-          } else {
-            st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
-            st.mant_median = st.mant_mean;
-          }
-          const bool acc_ok = (int)st.exp_mismatch <= th.max_exp_mismatch &&
-                              st.mant_mean <= th.max_mant_mean && st.mant_median <= th.max_mant_median;
-          st.flags = acc_ok ? TL_STAT_ACCEPT : 0u;
         }
-        if (stats_out) stats_out[j] = st;
-        accept_out[j] = (uint8_t)(st.flags & TL_STAT_ACCEPT);
+        const bool ok = (int)st.exp_mismatch <= th.max_exp_mismatch && st.mant_mean <= th.max_mant_mean &&
+                        st.mant_median <= th.max_mant_median;
+        st.flags = ok ? TL_STAT_ACCEPT : 0u;
       }
+      if (stats_out) stats_out[j] = st;
+      accept_out[j] = (uint8_t)(st.flags & TL_STAT_ACCEPT);
     }
-    csync();
+    __syncwarp();
+    PROF_MARK(4);
   }
+  spec_store(a.spec, gw, sp, lane);
+  PROF_FLUSH();
 }
 
 __global__ void rollout_verdict_kernel(const uint8_t* __restrict__ chunk_accept,
@@ -1269,11 +1069,12 @@ __global__ void synth_kernel(uint16_t* __restrict__ out, int64_t row0, int64_t n
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t prefix, tables, idx, bits, accept, total;
+  size_t spec, prefix, tables, idx, bits, accept, total;
 };
 WsLayout ws_layout(int32_t n_roll, int64_t n_chunks, int32_t K) {
   WsLayout L;
   size_t o = 0;
+  L.spec = o; o += (size_t)kSpecSlots * 16;  // first, so its offset never depends on the shape
   L.prefix = o; o = align_up(o + (size_t)(n_roll + 1) * 8, 256);
   L.tables = o; o = align_up(o + (size_t)kInvTables * 65536 * 2, 256);
   L.idx = o; o = align_up(o + (size_t)n_chunks * K * 4, 256);
@@ -1303,8 +1104,12 @@ int sel_grid(int64_t n_chunks, const void* kernel, int ctas_per_sm = 0) {
       per_sm < 1)
     per_sm = 1;
   if (ctas_per_sm > 0 && ctas_per_sm < per_sm) per_sm = ctas_per_sm;
-  const int64_t g = (int64_t)sm_count() * per_sm;
-  return (int)(n_chunks < g ? (n_chunks > 0 ? n_chunks : 1) : g);
+  // one warp per chunk: the fewest warps that finish in the same number of rounds
+  // as the full grid (fewer warps share HBM bandwidth, so each round is shorter)
+  const int64_t wmax = (int64_t)sm_count() * per_sm * kSelWarps;
+  const int64_t rounds = (n_chunks + wmax - 1) / wmax;
+  const int64_t warps = rounds > 0 ? (n_chunks + rounds - 1) / rounds : 1;
+  return (int)((warps + kSelWarps - 1) / kSelWarps);
 }
 
 int launch_status() { return cudaGetLastError() == cudaSuccess ? TL_OK : TL_ECUDA; }
@@ -1384,7 +1189,7 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   int64_t* prefix = reinterpret_cast<int64_t*>(ws + L.prefix);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix);
-  const SelArgs a{hidden, row_off, prefix, n_roll, H, C, K, n_chunks};
+  const SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec), n_roll, H, C, K, n_chunks};
   if (cudaFuncSetAttribute(prove_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
       cudaSuccess)
     return TL_ECUDA;
@@ -1393,6 +1198,17 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
       a, idx_out, bits_out);
   return launch_status();
 }
+
+#if TL_PHASE_PROF
+int tl_phase_prof(unsigned long long* out64, int reset) {
+  if (cudaMemcpyFromSymbol(out64, g_prof, sizeof(g_prof)) != cudaSuccess) return TL_ECUDA;
+  if (reset) {
+    static const unsigned long long z[16] = {};
+    if (cudaMemcpyToSymbol(g_prof, z, sizeof(z)) != cudaSuccess) return TL_ECUDA;
+  }
+  return TL_OK;
+}
+#endif
 
 int tl_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_t K,
               uint8_t* proofs_out, void* workspace, size_t workspace_bytes, void* stream) {
@@ -1469,7 +1285,7 @@ int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
 
   chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix);
   if (n_chunks > 0) {
-    const SelArgs a{hidden, row_off, prefix, n_roll, H, C, K, n_chunks};
+    const SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec), n_roll, H, C, K, n_chunks};
     if (cudaFuncSetAttribute(verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
         cudaSuccess)
       return TL_ECUDA;

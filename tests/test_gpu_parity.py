@@ -154,6 +154,44 @@ def test_prove_many_chunks_mixed_distributions():
     check_prove_against_oracle(bits, offs)
 
 
+def test_speculation_state_is_only_a_hint():
+    """The per-warp threshold speculation persists in the workspace between launches
+    (csrc/toploc_b200.cu, spec_load/spec_store: 16-byte slots at offset 0).  Whatever
+    the slots hold -- garbage, thresholds far too high (every chunk re-scanned),
+    zero, or plausible values -- select and verify stay bit-exact."""
+    H, C, K = 1024, 32, 128
+    n_chunks = 600
+    bits = np.concatenate([synth_bits(j * C, C, H, seed=j % 3, dist=[0, 1, 3][j % 3]) for j in range(n_chunks)])
+    offs = list(range(0, n_chunks * C + 1, C * 40))
+    _, chunks = TO._chunks_of(bits, offs, C)
+    idxs, vals, proofs = TO.prove_chunks(chunks, K)
+    h = torch.from_numpy(bits.view(np.int16)).cuda()
+    plan = api.engine().plan(offs, H)
+    slots = plan.ws[:8192 * 16].view(torch.int32).view(-1, 4)
+    magic = 0x53504543
+    g = torch.Generator(device="cpu").manual_seed(7)
+    fills = {
+        "garbage": torch.randint(-2**31, 2**31 - 1, tuple(slots.shape), generator=g, dtype=torch.int32),
+        "too_high": torch.tensor([0x7FFF, 0x7FFF, 1, magic], dtype=torch.int32),
+        "zero": torch.tensor([0, 0, 1, magic], dtype=torch.int32),
+        "plausible": torch.tensor([0x4050, 0x4070, 40, magic], dtype=torch.int32),
+    }
+    for name, fill in fills.items():
+        slots[:] = fill.cuda()
+        plan.select(h)
+        gi = plan.idx.cpu().numpy()
+        gv = plan.bits.cpu().numpy().view(np.uint16)
+        for j in range(n_chunks):
+            assert np.array_equal(gi[j], idxs[j]) and np.array_equal(gv[j], vals[j]), f"{name}: chunk {j}"
+        plan.commit()
+        assert all(plan.proofs[j].cpu().numpy().tobytes() == proofs[j] for j in range(n_chunks)), name
+        slots[:] = fill.cuda()
+        plan.verify(h)
+        assert bool(plan.chunk_accept.all()), name
+        st = plan.stats.cpu().numpy().view(np.uint32).reshape(n_chunks, 8)
+        assert np.all(st[:, 0] == 0) and np.all(st[:, 1] == K), name
+
+
 def test_prove_collisions_use_fallback_primes():
     H = 5120
     bits = synth_bits(0, 32 * 60, H, seed=5, dist=0)
