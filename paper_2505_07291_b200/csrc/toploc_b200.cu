@@ -209,10 +209,23 @@ __device__ __forceinline__ void spec_store(uint4* slots, int64_t gw, const Spec&
 // and counters (5 chunks, 6 candidates, 7 re-scanned chunks), 8 theta = 0 passes;
 // read by tl_phase_prof.
 __device__ unsigned long long g_prof[16];
-#define PROF_DECL unsigned long long prof_[16] = {}; long long prof_last_ = clock64()
+__device__ unsigned long long g_prof_warp[8192][2];  // per global warp: globaltimer at start / end (ns)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROF_DECL unsigned long long prof_[16] = {}; long long prof_last_ = clock64(); const unsigned long long prof_t0_ = gtimer()
 #define PROF_MARK(ph) do { const long long t_ = clock64(); prof_[ph] += t_ - prof_last_; prof_last_ = t_; } while (0)
 #define PROF_COUNT(i, v) (prof_[i] += (v))
-#define PROF_FLUSH() do { if ((threadIdx.x & 31) == 0) for (int q_ = 0; q_ < 16; ++q_) atomicAdd(&g_prof[q_], prof_[q_]); } while (0)
+#define PROF_FLUSH()                                                                            \
+  do {                                                                                          \
+    if ((threadIdx.x & 31) == 0) {                                                              \
+      for (int q_ = 0; q_ < 16; ++q_) atomicAdd(&g_prof[q_], prof_[q_]);                        \
+      const int64_t w_ = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5);                  \
+      if (w_ < 8192) { g_prof_warp[w_][0] = prof_t0_; g_prof_warp[w_][1] = gtimer(); }          \
+    }                                                                                           \
+  } while (0)
 #define PROF_ARG , unsigned long long (&prof_)[16], long long& prof_last_
 #define PROF_PASS , prof_, prof_last_
 #else
@@ -251,9 +264,19 @@ struct SelArgs {
   const int64_t* row_off;
   const int64_t* prefix;
   uint4* spec;       // workspace: speculation state per warp slot, kept across launches
+  unsigned long long* next;  // workspace: chunks handed out beyond the first round (reset by chunk_prefix_kernel)
   int n_roll, H, C, K;
   int64_t n_chunks;  // caller's n_chunks (clamped to prefix[n_roll] in the kernels)
 };
+// Chunk scheduling: the first round is static (chunk = global warp id), later chunks
+// are claimed from a workspace counter, so warps that stream faster (SMs with fewer
+// resident CTAs, better HBM placement) take more chunks and all warps finish within
+// about one chunk of each other.  Lane 0 claims at the chunk start; the claim is
+// broadcast at the chunk end, so the atomic's latency hides behind the chunk.
+__device__ __forceinline__ unsigned long long claim_chunk(const SelArgs& a, int lane) {
+  return lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;
+}
+
 __device__ __forceinline__ ChunkGeo chunk_geo(const SelArgs& a, int64_t j) {
   const ChunkRef cr = locate_chunk(a.prefix, a.row_off, a.n_roll, j, a.C);
   ChunkGeo g;
@@ -524,11 +547,11 @@ __device__ int select_chunk(const ChunkGeo& cg, int kk, WarpSlot& slot, Spec& sp
 
 // ----------------------------------------------------------------------------- kernels
 __global__ void chunk_prefix_kernel(const int64_t* __restrict__ row_off, int n_roll, int C,
-                                    int64_t* __restrict__ prefix) {
+                                    int64_t* __restrict__ prefix, unsigned long long* __restrict__ next_chunk) {
   __shared__ int64_t warp_tot[32];
   __shared__ int64_t carry;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid == 0) { carry = 0; prefix[0] = 0; }
+  if (tid == 0) { carry = 0; prefix[0] = 0; *next_chunk = 0; }
   __syncthreads();
   for (int base = 0; base < n_roll; base += blockDim.x) {
     const int r = base + tid;
@@ -574,7 +597,8 @@ prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restri
   const int64_t gw = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5);
   Spec sp = spec_load(a.spec, gw);
   PROF_DECL;
-  for (int64_t j = gw; j < n_chunks; j += nw) {
+  for (int64_t j = gw; j < n_chunks;) {
+    const unsigned long long claim = claim_chunk(a, lane);
     const ChunkGeo g = chunk_geo(a, j);
     const int kk = min(K, g.n);
     PROF_MARK(0);
@@ -591,6 +615,7 @@ prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restri
     }
     __syncwarp();
     PROF_MARK(4);
+    j = nw + (int64_t)__shfl_sync(0xFFFFFFFFu, claim, 0);
   }
   spec_store(a.spec, gw, sp, lane);
   PROF_FLUSH();
@@ -720,11 +745,86 @@ __device__ __forceinline__ void interpolate_warp(const uint32_t (&x)[4], uint32_
   conv_steps<3>(kk - 97, 0, poly, xs, cs, m, lane);
 }
 
-// One warp per chunk: modulus search, GF(p) interpolation, 258-byte serialisation.
-// WARPS x 32 threads, one CTA per SM.  HALF = 64 KiB half inverse table and <= 64
-// registers, so the CTA fits on an SM beside three select/verify CTAs (overlap mode).
+// One warp commits one chunk: modulus search, GF(p) interpolation and the 258-byte
+// serialisation.  The chunk's kk selected (flat index, bf16 bits) pairs are
+// raw[r], yb[r] at i = lane + 32 r (raw = 0xFFFFFFFF past kk).  MODE0 is the
+// inverse source for the first prime (tab0); primes 2..8 use the global tables,
+// later ones Fermat.  xs / cs: 128-word per-warp shared scratch.
+template <int MODE0>
+__device__ __forceinline__ void commit_chunk(const uint32_t (&raw)[4], const uint32_t (&yb)[4], int kk, int K,
+                                             const uint16_t* tab0, const uint16_t* __restrict__ inv_tables,
+                                             uint32_t* xs, uint32_t* cs, uint8_t* __restrict__ pr, int lane) {
+  const int PB = 2 + 2 * K;
+  uint32_t maxidx = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    if (lane + 32 * r < kk) maxidx = max(maxidx, raw[r]);
+  maxidx = __reduce_max_sync(0xFFFFFFFFu, maxidx);
+
+  // ---- modulus: largest prime with injective residues
+  int pi = 0;
+  uint32_t p = kPMax;
+  if (maxidx >= kPMax) {
+    for (pi = 0; pi < TL_N_PRIMES; ++pi) {
+      p = kPrimesDesc[pi];
+      const ModP mp(p);
+      uint32_t res[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = lane + 32 * r;
+        res[r] = (i < kk) ? mp.red(raw[r]) : 0x10000u + (uint32_t)i;
+      }
+      warp_sort128(res, lane);
+      bool dup = false;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, res[r], 1);
+        const uint32_t first_next = __shfl_sync(0xFFFFFFFFu, res[r < 3 ? r + 1 : 3], 0);
+        if (lane == 31) nxt = (r < 3) ? first_next : 0xFFFFFFFFu;
+        dup |= (nxt == res[r]);
+      }
+      if (!__any_sync(0xFFFFFFFFu, dup)) break;
+    }
+    if (pi == TL_N_PRIMES) p = 0;
+  }
+  if (p == 0) {  // unprovable chunk: p = 0, zero coefficients
+    for (int b = lane; b < PB; b += 32) pr[b] = 0;
+    return;
+  }
+  const ModP m(p);
+  uint32_t x[4], c[4], poly[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = lane + 32 * r;
+    x[r] = (i < kk) ? m.red(raw[r]) : 0u;
+    c[r] = (i < kk) ? m.red(yb[r]) : 0u;
+    xs[i] = x[r];
+  }
+  __syncwarp();
+  if (pi == 0) interpolate_warp<MODE0>(x, c, poly, xs, cs, kk, m, tab0, lane);
+  else if (pi < kInvTables) interpolate_warp<kInvGlobal>(x, c, poly, xs, cs, kk, m, inv_tables + (size_t)pi * 65536u, lane);
+  else interpolate_warp<kInvFermat>(x, c, poly, xs, cs, kk, m, nullptr, lane);
+
+  // ---- serialise: p, c_0..c_{K-1}, u16 big-endian
+  uint16_t* pw = reinterpret_cast<uint16_t*>(pr);
+  if (lane == 0) pw[0] = (uint16_t)(((p & 0xFFu) << 8) | (p >> 8));
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int k = lane + 32 * r;
+    if (k < K) {
+      const uint32_t v = poly[r];
+      pw[1 + k] = (uint16_t)(((v & 0xFFu) << 8) | (v >> 8));
+    }
+  }
+  __syncwarp();
+}
+
+// tl_commit: one warp per chunk over (idx, bits) in global memory.  WARPS x 32
+// threads, one CTA per SM, the first prime's inverse table staged in shared memory
+// (HALF = 64 KiB half table and <= 64 registers, so the CTA fits beside three
+// select/verify CTAs for the overlapped pipeline).
 template <int WARPS, bool HALF>
-__global__ void __launch_bounds__(WARPS * 32, HALF ? 4 : (WARPS > 16 ? 1 : 1))
+__global__ void __launch_bounds__(WARPS * 32, HALF ? 4 : 1)
 commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits, int64_t n_chunks,
               int K, const uint16_t* __restrict__ inv_tables, uint8_t* __restrict__ proofs) {
   constexpr int kTabEntries = HALF ? kHalfTab : 65536;
@@ -742,11 +842,9 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
   uint32_t* xs = xs_all + warp * 128;
   uint32_t* cs = cs_all + warp * 128;
   const int PB = 2 + 2 * K;
-
   for (int64_t j = (int64_t)blockIdx.x * WARPS + warp; j < n_chunks; j += (int64_t)gridDim.x * WARPS) {
     uint32_t raw[4], yb[4];
     int kk = 0;
-    uint32_t maxidx = 0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int i = lane + 32 * r;
@@ -756,71 +854,11 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
       raw[r] = (uint32_t)iv;
       yb[r] = b;
       kk += __popc(__ballot_sync(0xFFFFFFFFu, iv >= 0));
-      if (iv >= 0) maxidx = max(maxidx, (uint32_t)iv);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) maxidx = max(maxidx, __shfl_xor_sync(0xFFFFFFFFu, maxidx, o));
-
-    // ---- modulus: largest prime with injective residues
-    int pi = 0;
-    uint32_t p = kPMax;
-    if (maxidx >= kPMax) {
-      for (pi = 0; pi < TL_N_PRIMES; ++pi) {
-        p = kPrimesDesc[pi];
-        const ModP mp(p);
-        uint32_t res[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int i = lane + 32 * r;
-          res[r] = (i < kk) ? mp.red(raw[r]) : 0x10000u + (uint32_t)i;
-        }
-        warp_sort128(res, lane);
-        bool dup = false;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, res[r], 1);
-          const uint32_t first_next = __shfl_sync(0xFFFFFFFFu, res[r < 3 ? r + 1 : 3], 0);
-          if (lane == 31) nxt = (r < 3) ? first_next : 0xFFFFFFFFu;
-          dup |= (nxt == res[r]);
-        }
-        if (!__any_sync(0xFFFFFFFFu, dup)) break;
-      }
-      if (pi == TL_N_PRIMES) p = 0;
-    }
-    uint8_t* pr = proofs + j * PB;
-    if (p == 0) {  // unprovable chunk: p = 0, zero coefficients
-      for (int b = lane; b < PB; b += 32) pr[b] = 0;
-      continue;
-    }
-    const ModP m(p);
-    uint32_t x[4], c[4], poly[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int i = lane + 32 * r;
-      x[r] = (i < kk) ? m.red(raw[r]) : 0u;
-      c[r] = (i < kk) ? m.red(yb[r]) : 0u;
-      xs[i] = x[r];
-    }
-    __syncwarp();
-    if (pi == 0) interpolate_warp<HALF ? kInvSmemHalf : kInvSmem>(x, c, poly, xs, cs, kk, m, inv0, lane);
-    else if (pi < kInvTables)
-      interpolate_warp<kInvGlobal>(x, c, poly, xs, cs, kk, m, inv_tables + (size_t)pi * 65536u, lane);
-    else interpolate_warp<kInvFermat>(x, c, poly, xs, cs, kk, m, nullptr, lane);
-
-    // ---- serialise: p, c_0..c_{K-1}, u16 big-endian
-    uint16_t* pw = reinterpret_cast<uint16_t*>(pr);
-    if (lane == 0) pw[0] = (uint16_t)(((p & 0xFFu) << 8) | (p >> 8));
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int k = lane + 32 * r;
-      if (k < K) {
-        const uint32_t v = poly[r];
-        pw[1 + k] = (uint16_t)(((v & 0xFFu) << 8) | (v >> 8));
-      }
-    }
-    __syncwarp();
+    commit_chunk<HALF ? kInvSmemHalf : kInvSmem>(raw, yb, kk, K, inv0, inv_tables, xs, cs, proofs + j * PB, lane);
   }
 }
+
 
 // Verify: the warp selects its chunk's top-kk on the validator tensor, evaluates
 // the claimed polynomial at the kk indices (Horner, four points per lane),
@@ -842,7 +880,8 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
   const int64_t gw = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5);
   Spec sp = spec_load(a.spec, gw);
   PROF_DECL;
-  for (int64_t j = gw; j < n_chunks; j += nw) {
+  for (int64_t j = gw; j < n_chunks;) {
+    const unsigned long long claim = claim_chunk(a, lane);
     const ChunkGeo g = chunk_geo(a, j);
     const int kk = min(K, g.n);
     // issue this chunk's proof loads (u16 t = p or c_{t-1}) before streaming, so
@@ -959,6 +998,7 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
     }
     __syncwarp();
     PROF_MARK(4);
+    j = nw + (int64_t)__shfl_sync(0xFFFFFFFFu, claim, 0);
   }
   spec_store(a.spec, gw, sp, lane);
   PROF_FLUSH();
@@ -1069,12 +1109,13 @@ __global__ void synth_kernel(uint16_t* __restrict__ out, int64_t row0, int64_t n
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t spec, prefix, tables, idx, bits, accept, total;
+  size_t spec, next, prefix, tables, idx, bits, accept, total;
 };
 WsLayout ws_layout(int32_t n_roll, int64_t n_chunks, int32_t K) {
   WsLayout L;
   size_t o = 0;
   L.spec = o; o += (size_t)kSpecSlots * 16;  // first, so its offset never depends on the shape
+  L.next = o; o += 256;                       // dynamic chunk counter of the streaming kernels
   L.prefix = o; o = align_up(o + (size_t)(n_roll + 1) * 8, 256);
   L.tables = o; o = align_up(o + (size_t)kInvTables * 65536 * 2, 256);
   L.idx = o; o = align_up(o + (size_t)n_chunks * K * 4, 256);
@@ -1188,8 +1229,10 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   int64_t* prefix = reinterpret_cast<int64_t*>(ws + L.prefix);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix);
-  const SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec), n_roll, H, C, K, n_chunks};
+  chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix,
+                                          reinterpret_cast<unsigned long long*>(ws + L.next));
+  const SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
+                  reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
   if (cudaFuncSetAttribute(prove_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
       cudaSuccess)
     return TL_ECUDA;
@@ -1200,6 +1243,9 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
 }
 
 #if TL_PHASE_PROF
+int tl_phase_prof_warps(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_prof_warp, sizeof(g_prof_warp)) == cudaSuccess ? TL_OK : TL_ECUDA;
+}
 int tl_phase_prof(unsigned long long* out64, int reset) {
   if (cudaMemcpyFromSymbol(out64, g_prof, sizeof(g_prof)) != cudaSuccess) return TL_ECUDA;
   if (reset) {
@@ -1283,9 +1329,11 @@ int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   uint8_t* accept = chunk_accept_out ? chunk_accept_out : ws + L.accept;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
-  chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix);
+  chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix,
+                                          reinterpret_cast<unsigned long long*>(ws + L.next));
   if (n_chunks > 0) {
-    const SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec), n_roll, H, C, K, n_chunks};
+    const SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
+                  reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
     if (cudaFuncSetAttribute(verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
         cudaSuccess)
       return TL_ECUDA;

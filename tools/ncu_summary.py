@@ -3,8 +3,9 @@
     python tools/ncu_summary.py gpurun_out/prof.ncu-rep gpurun_out/launches.csv profiles/rNN [bench.json]
 
 Writes <prefix>_ncu_summary.md (per-kernel metrics from the --set full capture and the
-launch list of the same bench command) and profiles/ncu_select_traffic.json (DRAM
-bytes per tl_select launch, read by bench.py for roofline.traffic)."""
+launch list of the same bench command) and profiles/ncu_prove_traffic.json /
+ncu_select_traffic.json (DRAM bytes per tl_prove / tl_select launch, read by bench.py
+for roofline.traffic)."""
 import csv
 import io
 import json
@@ -36,7 +37,7 @@ WANT = [
 out = [f"# ncu summary ({os.path.basename(rep)})", "",
        "Captured with `ncu --set full --clock-control none --import-source on` on one B200 "
        "(cold, serialised replays: compare shares, not absolute times).", ""]
-traffic = {}
+traffic = {}  # per streaming kernel
 for r in rows[2:]:
     name = r[hdr.index("Kernel Name")]
     short = name.split("(")[0].split("::")[-1]
@@ -60,12 +61,12 @@ for r in rows[2:]:
     out.append("")
     out.append("Warp stall samples: " + ", ".join(f"{k} {v / tot * 100:.1f}%" for k, v in top))
     out.append("")
-    if "prove_select" in short:
+    if short.split("<")[0] in ("prove_kernel", "prove_select_kernel"):
         def gbytes(key):
             i = hdr.index(key)
             v = float(r[i])
             return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(units[i], 1.0)
-        traffic = {"kernel": short, "dram_bytes_per_launch": gbytes("dram__bytes_read.sum") + gbytes("dram__bytes_write.sum"),
+        traffic[short.split("<")[0]] = {"kernel": short, "dram_bytes_per_launch": gbytes("dram__bytes_read.sum") + gbytes("dram__bytes_write.sum"),
                    "config": "cfg2", "source": os.path.basename(rep)}
 # launch list
 lrows = list(csv.reader(open(launches)))
@@ -80,20 +81,22 @@ for r in lrows[hi + 1:]:
     per.setdefault(k, []).append(float(r[vi].replace(",", "")) * (1e-6 if r[ui] == "ns" else 1e-3 if r[ui] == "us" else 1.0))
 out.append("## Launch list (same bench command, `--metrics gpu__time_duration.sum --clock-control none`)")
 out.append("")
-out.append("| kernel | launches | mean ms | share of select+commit+verify |")
+out.append("| kernel | launches | mean ms | share of the step's main kernels |")
 out.append("|---|---|---|---|")
-step = sum(sum(v) / len(v) for k, v in per.items() if k in ("prove_select_kernel", "commit_kernel", "verify_kernel"))
+STEP = ("prove_kernel", "prove_select_kernel", "commit_kernel", "verify_kernel")
+step = sum(sum(v) / len(v) for k, v in per.items() if k in STEP)
 for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
     m = sum(v) / len(v)
-    share = f"{m / step * 100:.1f}%" if k in ("prove_select_kernel", "commit_kernel", "verify_kernel") and step else ""
+    share = f"{m / step * 100:.1f}%" if k in STEP and step else ""
     out.append(f"| {k} | {len(v)} | {m:.4f} | {share} |")
 if bench:
     out.append("")
     ph = bench.get("phases_ms", {})
-    live = ph.get("select", 0) + ph.get("commit", 0) + ph.get("verify", 0)
-    out.append("Live (CUDA events, bench.py) shares: " + ", ".join(
-        f"{k} {ph[k] / live * 100:.1f}%" for k in ("select", "commit", "verify") if k in ph))
+    keys = [k for k in ("prove", "select", "commit", "verify") if isinstance(ph.get(k), (int, float))]
+    live = sum(ph[k] for k in keys)
+    out.append("Live (CUDA events, bench.py) shares: " + ", ".join(f"{k} {ph[k] / live * 100:.1f}%" for k in keys))
 open(prefix + "_ncu_summary.md", "w").write("\n".join(out) + "\n")
-if traffic:
-    json.dump(traffic, open(os.path.join(os.path.dirname(prefix), "ncu_select_traffic.json"), "w"), indent=1)
+for name, fn in (("prove_kernel", "ncu_prove_traffic.json"), ("prove_select_kernel", "ncu_select_traffic.json")):
+    if name in traffic:
+        json.dump(traffic[name], open(os.path.join(os.path.dirname(prefix), fn), "w"), indent=1)
 print("\n".join(out))
