@@ -28,7 +28,7 @@ namespace {
 
 // ----------------------------------------------------------------------------- constants
 #ifndef TL_SEL_THREADS
-#define TL_SEL_THREADS 96
+#define TL_SEL_THREADS 32  // one warp per CTA: 28 independent streaming warps per SM (see DESIGN 5.1)
 #endif
 constexpr int kSelThreads = TL_SEL_THREADS;   // select CTA threads (independent warps)
 #ifndef TL_SEL_U
@@ -36,7 +36,7 @@ constexpr int kSelThreads = TL_SEL_THREADS;   // select CTA threads (independent
 #endif
 constexpr int kSelU = TL_SEL_U;               // 16-B vectors per lane per warp tile
 #ifndef TL_SEL_MIN_BLOCKS
-#define TL_SEL_MIN_BLOCKS 8
+#define TL_SEL_MIN_BLOCKS 28
 #endif
 constexpr int kSelMinBlocks = TL_SEL_MIN_BLOCKS;  // resident select CTAs per SM
 constexpr int kSelWarps = kSelThreads / 32;
