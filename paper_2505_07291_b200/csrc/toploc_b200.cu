@@ -28,15 +28,15 @@ namespace {
 
 // ----------------------------------------------------------------------------- constants
 #ifndef TL_SEL_THREADS
-#define TL_SEL_THREADS 32  // one warp per CTA: 28 independent streaming warps per SM (see DESIGN 5.1)
+#define TL_SEL_THREADS 32  // one warp per CTA: independent streaming warps (see DESIGN 5.1)
 #endif
 constexpr int kSelThreads = TL_SEL_THREADS;   // select CTA threads (independent warps)
 #ifndef TL_SEL_U
-#define TL_SEL_U 4
+#define TL_SEL_U 8
 #endif
 constexpr int kSelU = TL_SEL_U;               // 16-B vectors per lane per warp tile
 #ifndef TL_SEL_MIN_BLOCKS
-#define TL_SEL_MIN_BLOCKS 28
+#define TL_SEL_MIN_BLOCKS 18
 #endif
 constexpr int kSelMinBlocks = TL_SEL_MIN_BLOCKS;  // resident select CTAs per SM
 constexpr int kSelWarps = kSelThreads / 32;
@@ -45,10 +45,10 @@ static_assert(kWarpCap >= TL_MAX_K + 32, "a compaction must leave room for one f
 constexpr int kFlushAt = 4;                   // flagged vectors per exact-test round (32 lanes / 8)
 constexpr int kStageVec = 32 * kSelU + 8;     // per-warp flagged-vector queue (< kFlushAt pending + a tile)
 #ifndef TL_SPEC_LO
-#define TL_SPEC_LO 16   // adapt the margin so a chunk yields kk + [LO, HI] candidates
+#define TL_SPEC_LO 32   // adapt the margin so a chunk yields kk + [LO, HI] candidates
 #endif
 #ifndef TL_SPEC_HI
-#define TL_SPEC_HI 96   // < kWarpCap - TL_MAX_K: no compaction at the target
+#define TL_SPEC_HI 112  // < kWarpCap - TL_MAX_K: no compaction at the target
 #endif
 constexpr unsigned kIdxMask = 0xFFFFFFu;      // flat index field (24 bits)
 constexpr int kInvTables = 8;                 // precomputed inverse tables (first 8 primes)
