@@ -84,10 +84,10 @@ out.append("")
 out.append("| kernel | launches | mean ms | share of the step's main kernels |")
 out.append("|---|---|---|---|")
 STEP = ("prove_kernel", "prove_select_kernel", "commit_kernel", "verify_kernel")
-step = sum(sum(v) / len(v) for k, v in per.items() if k in STEP)
+step = sum(sum(v) / len(v) for k, v in per.items() if k.split("<")[0] in STEP)
 for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
     m = sum(v) / len(v)
-    share = f"{m / step * 100:.1f}%" if k in STEP and step else ""
+    share = f"{m / step * 100:.1f}%" if k.split("<")[0] in STEP and step else ""
     out.append(f"| {k} | {len(v)} | {m:.4f} | {share} |")
 if bench:
     out.append("")
