@@ -52,6 +52,8 @@ constexpr int kStageVec = 32 * kSelU + 8;     // per-warp flagged-vector queue (
 #endif
 constexpr unsigned kIdxMask = 0xFFFFFFu;      // flat index field (24 bits)
 constexpr int kInvTables = 8;                 // precomputed inverse tables (first 8 primes)
+constexpr int kHashBits = 8;                  // injectivity check: 256-slot set per commit warp
+constexpr int kHashSlots = 1 << kHashBits;
 constexpr int kSpecSlots = 8192;              // speculation slots in the workspace (16 B each)
 #ifndef TL_COMMIT_WARPS
 #define TL_COMMIT_WARPS 32
@@ -621,41 +623,9 @@ prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restri
   PROF_FLUSH();
 }
 
-// Warp-wide bitonic sort (ascending over i = lane + 32 r) of 4 registers per lane.
-__device__ __forceinline__ void warp_sort128(uint32_t (&v)[4], int lane) {
-#pragma unroll
-  for (int k = 2; k <= 128; k <<= 1) {
-#pragma unroll
-    for (int jj = k >> 1; jj > 0; jj >>= 1) {
-      if (jj >= 32) {
-        const int rj = jj >> 5;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          if ((r & rj) == 0) {
-            const int i = lane + 32 * r;
-            const bool asc = (i & k) == 0;
-            const uint32_t a = v[r], b = v[r | rj];
-            const uint32_t lo = min(a, b), hi = max(a, b);
-            v[r] = asc ? lo : hi;
-            v[r | rj] = asc ? hi : lo;
-          }
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, v[r], jj);
-          const int i = lane + 32 * r;
-          const bool asc = (i & k) == 0;
-          const bool lower = (lane & jj) == 0;
-          v[r] = (asc == lower) ? min(v[r], o) : max(v[r], o);
-        }
-      }
-    }
-  }
-}
-
-__global__ void inv_table_kernel(uint16_t* __restrict__ tables) {
+__global__ void inv_table_kernel(uint16_t* __restrict__ tables, unsigned long long* __restrict__ next) {
   const int q = blockIdx.y;
+  if (next && blockIdx.x == 0 && q == 0 && threadIdx.x == 0) *next = 0;  // commit_kernel's chunk counter
   const uint32_t p = kPrimesDesc[q];
   const ModP m(p);
   for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < 65536u; a += gridDim.x * blockDim.x)
@@ -750,10 +720,37 @@ __device__ __forceinline__ void interpolate_warp(const uint32_t (&x)[4], uint32_
 // raw[r], yb[r] at i = lane + 32 r (raw = 0xFFFFFFFF past kk).  MODE0 is the
 // inverse source for the first prime (tab0); primes 2..8 use the global tables,
 // later ones Fermat.  xs / cs: 128-word per-warp shared scratch.
+// True iff the warp's kk residues res[r] (i = lane + 32 r < kk, each < 2^16) are
+// pairwise distinct: insert into a 256-slot open-addressing set in shared memory
+// (hs, per warp) with atomicCAS; an insert that finds its own value is a duplicate.
+__device__ __forceinline__ bool residues_distinct(const uint32_t (&res)[4], int kk, uint32_t* hs, int lane) {
+#pragma unroll
+  for (int q = 0; q < kHashSlots / 32; ++q) hs[lane + 32 * q] = 0xFFFFFFFFu;
+  __syncwarp();
+  bool dup = false;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    if (lane + 32 * r < kk) {
+      const uint32_t v = res[r];
+      uint32_t h = (v * 0x9E3779B1u) >> (32 - kHashBits);
+      for (;;) {  // load <= 1/2: ~1.5 probes on average
+        const uint32_t old = atomicCAS(&hs[h], 0xFFFFFFFFu, v);
+        if (old == 0xFFFFFFFFu) break;
+        if (old == v) { dup = true; break; }
+        h = (h + 1) & (kHashSlots - 1);
+      }
+    }
+  }
+  const bool any_dup = __any_sync(0xFFFFFFFFu, dup);
+  __syncwarp();
+  return !any_dup;
+}
+
 template <int MODE0>
 __device__ __forceinline__ void commit_chunk(const uint32_t (&raw)[4], const uint32_t (&yb)[4], int kk, int K,
                                              const uint16_t* tab0, const uint16_t* __restrict__ inv_tables,
-                                             uint32_t* xs, uint32_t* cs, uint8_t* __restrict__ pr, int lane) {
+                                             uint32_t* xs, uint32_t* cs, uint32_t* hs, uint8_t* __restrict__ pr,
+                                             int lane) {
   const int PB = 2 + 2 * K;
   uint32_t maxidx = 0;
 #pragma unroll
@@ -770,20 +767,8 @@ __device__ __forceinline__ void commit_chunk(const uint32_t (&raw)[4], const uin
       const ModP mp(p);
       uint32_t res[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int i = lane + 32 * r;
-        res[r] = (i < kk) ? mp.red(raw[r]) : 0x10000u + (uint32_t)i;
-      }
-      warp_sort128(res, lane);
-      bool dup = false;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, res[r], 1);
-        const uint32_t first_next = __shfl_sync(0xFFFFFFFFu, res[r < 3 ? r + 1 : 3], 0);
-        if (lane == 31) nxt = (r < 3) ? first_next : 0xFFFFFFFFu;
-        dup |= (nxt == res[r]);
-      }
-      if (!__any_sync(0xFFFFFFFFu, dup)) break;
+      for (int r = 0; r < 4; ++r) res[r] = mp.red(raw[r]);
+      if (residues_distinct(res, kk, hs, lane)) break;
     }
     if (pi == TL_N_PRIMES) p = 0;
   }
@@ -826,12 +811,14 @@ __device__ __forceinline__ void commit_chunk(const uint32_t (&raw)[4], const uin
 template <int WARPS, bool HALF>
 __global__ void __launch_bounds__(WARPS * 32, HALF ? 4 : 1)
 commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits, int64_t n_chunks,
-              int K, const uint16_t* __restrict__ inv_tables, uint8_t* __restrict__ proofs) {
+              int K, const uint16_t* __restrict__ inv_tables, uint8_t* __restrict__ proofs,
+              unsigned long long* __restrict__ next) {
   constexpr int kTabEntries = HALF ? kHalfTab : 65536;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint16_t* inv0 = reinterpret_cast<uint16_t*>(smem_raw);
   uint32_t* xs_all = reinterpret_cast<uint32_t*>(smem_raw + kTabEntries * 2);  // [warps][128]
   uint32_t* cs_all = xs_all + WARPS * 128;                                     // [warps][128]
+  uint32_t* hs_all = cs_all + WARPS * 128;                                     // [warps][kHashSlots]
   {
     const uint4* src = reinterpret_cast<const uint4*>(inv_tables);
     uint4* dst = reinterpret_cast<uint4*>(inv0);
@@ -841,8 +828,12 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* xs = xs_all + warp * 128;
   uint32_t* cs = cs_all + warp * 128;
+  uint32_t* hs = hs_all + warp * kHashSlots;
   const int PB = 2 + 2 * K;
-  for (int64_t j = (int64_t)blockIdx.x * WARPS + warp; j < n_chunks; j += (int64_t)gridDim.x * WARPS) {
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  // first round static, then chunks claimed from the counter (reset by inv_table_kernel)
+  for (int64_t j = (int64_t)blockIdx.x * WARPS + warp; j < n_chunks;) {
+    const unsigned long long claim = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
     uint32_t raw[4], yb[4];
     int kk = 0;
 #pragma unroll
@@ -855,7 +846,9 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
       yb[r] = b;
       kk += __popc(__ballot_sync(0xFFFFFFFFu, iv >= 0));
     }
-    commit_chunk<HALF ? kInvSmemHalf : kInvSmem>(raw, yb, kk, K, inv0, inv_tables, xs, cs, proofs + j * PB, lane);
+    commit_chunk<HALF ? kInvSmemHalf : kInvSmem>(raw, yb, kk, K, inv0, inv_tables, xs, cs, hs, proofs + j * PB,
+                                                 lane);
+    j = nw + (int64_t)__shfl_sync(0xFFFFFFFFu, claim, 0);
   }
 }
 
@@ -1115,7 +1108,7 @@ WsLayout ws_layout(int32_t n_roll, int64_t n_chunks, int32_t K) {
   WsLayout L;
   size_t o = 0;
   L.spec = o; o += (size_t)kSpecSlots * 16;  // first, so its offset never depends on the shape
-  L.next = o; o += 256;                       // dynamic chunk counter of the streaming kernels
+  L.next = o; o += 256;                       // chunk counters: [0] streaming kernels, [1] commit
   L.prefix = o; o = align_up(o + (size_t)(n_roll + 1) * 8, 256);
   L.tables = o; o = align_up(o + (size_t)kInvTables * 65536 * 2, 256);
   L.idx = o; o = align_up(o + (size_t)n_chunks * K * 4, 256);
@@ -1157,23 +1150,23 @@ int launch_status() { return cudaGetLastError() == cudaSuccess ? TL_OK : TL_ECUD
 
 template <int WARPS, bool HALF>
 int launch_commit_t(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, const uint16_t* tables,
-                    uint8_t* proofs, cudaStream_t st) {
-  const size_t smem = (size_t)(HALF ? kHalfTab : 65536) * 2 + 2 * WARPS * 128 * 4;
+                    uint8_t* proofs, unsigned long long* next, cudaStream_t st) {
+  const size_t smem = (size_t)(HALF ? kHalfTab : 65536) * 2 + (2 * 128 + kHashSlots) * WARPS * 4;
   if (cudaFuncSetAttribute(commit_kernel<WARPS, HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return TL_ECUDA;
   int grid = sm_count();
   if ((int64_t)grid * WARPS > n_chunks) grid = (int)((n_chunks + WARPS - 1) / WARPS);
-  commit_kernel<WARPS, HALF><<<grid, WARPS * 32, smem, st>>>(idx, bits, n_chunks, K, tables, proofs);
+  commit_kernel<WARPS, HALF><<<grid, WARPS * 32, smem, st>>>(idx, bits, n_chunks, K, tables, proofs, next);
   return launch_status();
 }
 
 // co_resident = 0: 16 warps, full 128 KiB table (fastest alone); 1: 8 warps, 64 KiB
 // half table, <= 64 registers -- fits beside three select/verify CTAs per SM.
 int launch_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, const uint16_t* tables,
-                  uint8_t* proofs, int co_resident, cudaStream_t st) {
-  return co_resident ? launch_commit_t<8, true>(idx, bits, n_chunks, K, tables, proofs, st)
-                     : launch_commit_t<kCommitWarps, false>(idx, bits, n_chunks, K, tables, proofs, st);
+                  uint8_t* proofs, unsigned long long* next, int co_resident, cudaStream_t st) {
+  return co_resident ? launch_commit_t<8, true>(idx, bits, n_chunks, K, tables, proofs, next, st)
+                     : launch_commit_t<kCommitWarps, false>(idx, bits, n_chunks, K, tables, proofs, next, st);
 }
 
 }  // namespace
@@ -1258,17 +1251,7 @@ int tl_phase_prof(unsigned long long* out64, int reset) {
 
 int tl_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_t K,
               uint8_t* proofs_out, void* workspace, size_t workspace_bytes, void* stream) {
-  if (n_chunks < 0 || K < 1) return TL_EINVAL;
-  if (K > TL_MAX_K) return TL_EUNSUPPORTED;
-  if (n_chunks == 0) return TL_OK;
-  if (!idx || !bits || !proofs_out || !workspace) return TL_EINVAL;
-  const WsLayout L = ws_layout(0, n_chunks, K);
-  if (workspace_bytes < L.tables + (size_t)kInvTables * 65536 * 2 || (reinterpret_cast<uintptr_t>(workspace) & 255))
-    return TL_EWORKSPACE;
-  uint16_t* tables = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(workspace) + L.tables);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  inv_table_kernel<<<dim3(64, kInvTables), 256, 0, st>>>(tables);
-  return launch_commit(idx, bits, n_chunks, K, tables, proofs_out, 0, st);
+  return tl_commit_ex(idx, bits, n_chunks, K, proofs_out, workspace, workspace_bytes, 0, stream);
 }
 
 int tl_commit_ex(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_t K, uint8_t* proofs_out,
@@ -1280,10 +1263,12 @@ int tl_commit_ex(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int
   const WsLayout L = ws_layout(0, n_chunks, K);
   if (workspace_bytes < L.tables + (size_t)kInvTables * 65536 * 2 || (reinterpret_cast<uintptr_t>(workspace) & 255))
     return TL_EWORKSPACE;
-  uint16_t* tables = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(workspace) + L.tables);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  uint16_t* tables = reinterpret_cast<uint16_t*>(ws + L.tables);
+  unsigned long long* next = reinterpret_cast<unsigned long long*>(ws + L.next) + 1;  // commit's own counter
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  inv_table_kernel<<<dim3(64, kInvTables), 256, 0, st>>>(tables);
-  return launch_commit(idx, bits, n_chunks, K, tables, proofs_out, co_resident, st);
+  inv_table_kernel<<<dim3(64, kInvTables), 256, 0, st>>>(tables, next);
+  return launch_commit(idx, bits, n_chunks, K, tables, proofs_out, next, co_resident, st);
 }
 
 int tl_prove(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
