@@ -59,6 +59,14 @@ constexpr int kSpecSlots = 8192;              // speculation slots in the worksp
 #define TL_COMMIT_WARPS 32
 #endif
 constexpr int kCommitWarps = TL_COMMIT_WARPS;
+#ifndef TL_NDD_UNROLL
+#define TL_NDD_UNROLL 2  // divided-difference levels per loop iteration
+#endif
+#ifndef TL_CONV_UNROLL
+#define TL_CONV_UNROLL 2  // Newton -> monomial steps per loop iteration
+#endif
+constexpr int kNddUnroll = TL_NDD_UNROLL;
+constexpr int kConvUnroll = TL_CONV_UNROLL;
 constexpr uint32_t kPMax = 65497u;
 
 // ----------------------------------------------------------------------------- helpers
@@ -656,6 +664,7 @@ template <int MODE, int R0>
 __device__ __forceinline__ void ndd_levels(int j0, int j1, const uint32_t (&x)[4], uint32_t (&c)[4],
                                            const uint32_t* xs, const ModP& m, const uint16_t* tab, int lane) {
   const int src = (lane + 31) & 31;
+#pragma unroll kNddUnroll
   for (int jl = j0; jl < j1; ++jl) {
     uint32_t t[4];
 #pragma unroll
@@ -673,21 +682,22 @@ __device__ __forceinline__ void ndd_levels(int j0, int j1, const uint32_t (&x)[4
 
 // Newton -> monomial steps i in [i_lo, i_hi] (descending): poly <- poly * (X - x_i) + c_i.
 // The polynomial has degree kk-1-i <= 32 (RM + 1) - 1, so blocks r > RM stay zero.
+// nxs[i] = p - x_i.  Coefficient k takes prev_{k-1} + (p - x_i) a_k (< p^2 < 2^32); the
+// constant term's "previous" is c_i itself, which folds the + c_i into the same reduction.
 template <int RM>
-__device__ __forceinline__ void conv_steps(int i_hi, int i_lo, uint32_t (&poly)[4], const uint32_t* xs,
+__device__ __forceinline__ void conv_steps(int i_hi, int i_lo, uint32_t (&poly)[4], const uint32_t* nxs,
                                            const uint32_t* cs, const ModP& m, int lane) {
   const int src = (lane + 31) & 31;
+#pragma unroll kConvUnroll
   for (int i = i_hi; i >= i_lo; --i) {
-    const uint32_t nxi = m.p - xs[i], ci = cs[i];  // prevk - x_i a == prevk + (p - x_i) a < 2^32
+    const uint32_t nxi = nxs[i], ci = cs[i];
     uint32_t t[4];
 #pragma unroll
     for (int r = 0; r <= RM; ++r) t[r] = __shfl_sync(0xFFFFFFFFu, poly[r], src);
 #pragma unroll
     for (int r = 0; r <= RM; ++r) {
-      const uint32_t prevk = lane ? t[r] : (r ? t[r > 0 ? r - 1 : 0] : (0u));
-      uint32_t nv = m.red(prevk + nxi * poly[r]);
-      if (r == 0 && lane == 0) nv = m.add(nv, ci);
-      poly[r] = nv;
+      const uint32_t prevk = lane ? t[r] : (r ? t[r > 0 ? r - 1 : 0] : ci);
+      poly[r] = m.red(prevk + nxi * poly[r]);
     }
   }
 }
@@ -696,14 +706,18 @@ __device__ __forceinline__ void conv_steps(int i_hi, int i_lo, uint32_t (&poly)[
 // Newton divided differences, then Newton -> monomial.
 template <int MODE>
 __device__ __forceinline__ void interpolate_warp(const uint32_t (&x)[4], uint32_t (&c)[4], uint32_t (&poly)[4],
-                                                 const uint32_t* xs, uint32_t* cs, int kk, const ModP& m,
+                                                 uint32_t* xs, uint32_t* cs, int kk, const ModP& m,
                                                  const uint16_t* tab, int lane) {
   ndd_levels<MODE, 0>(1, min(kk, 32), x, c, xs, m, tab, lane);
   ndd_levels<MODE, 1>(32, min(kk, 64), x, c, xs, m, tab, lane);
   ndd_levels<MODE, 2>(64, min(kk, 96), x, c, xs, m, tab, lane);
   ndd_levels<MODE, 3>(96, kk, x, c, xs, m, tab, lane);
+  __syncwarp();  // every lane is done reading xs
 #pragma unroll
-  for (int r = 0; r < 4; ++r) cs[lane + 32 * r] = c[r];
+  for (int r = 0; r < 4; ++r) {
+    cs[lane + 32 * r] = c[r];
+    xs[lane + 32 * r] = m.p - x[r];  // the conversion multiplies by (X - x_i)
+  }
   __syncwarp();
 #pragma unroll
   for (int r = 0; r < 4; ++r) poly[r] = 0u;
