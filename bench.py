@@ -251,7 +251,7 @@ def run_b200(args, cfg, rank, world, local_rank):
             okp.append(pr[0] == got[j].tobytes())
         spot = {"chunks": js, "proofs_bit_exact": all(okp)}
 
-    pipe = api.Pipeline(eng, offs, H, ctas_per_sm=args.ctas) if args.pipeline else None
+    pipe = api.Pipeline(eng, offs, H, ctas_per_sm=args.ctas) if args.pipeline_on else None
     if pipe is not None:
         pipe.run([prv] * args.warmup, [val] * args.warmup)
         torch.cuda.synchronize(dev)
@@ -401,7 +401,7 @@ def run_b200(args, cfg, rank, world, local_rank):
                           "verify_gbs": ver_bytes / (ver_ms / 1e3) / 1e9, "verdict_gather": gather_ms,
                           "serial": serial_ms,
                           "schedule": (f"pipelined: commit(k) on a side stream overlaps verify(k-1); "
-                                       f"select/verify {args.ctas} CTAs/SM" if args.pipeline else "serial")},
+                                       f"select/verify {args.ctas} CTAs/SM" if args.pipeline_on else "serial")},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
@@ -426,9 +426,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-tokens", type=int, default=8192)
     ap.add_argument("--no-spot-check", dest="spot_check", action="store_false")
-    ap.add_argument("--pipeline", dest="pipeline", action="store_true")
-    ap.add_argument("--ctas", type=int, default=3, help="select/verify CTAs per SM in pipeline mode")
+    ap.add_argument("--schedule", default="pipeline", choices=["pipeline", "serial"],
+                    help="pipeline (default): commit(k) on a side stream overlaps verify(k-1) and select(k+1); "
+                         "serial: tl_select, tl_commit, tl_verify back to back")
+    ap.add_argument("--pipeline", dest="schedule", action="store_const", const="pipeline")
+    ap.add_argument("--serial", dest="schedule", action="store_const", const="serial")
+    ap.add_argument("--ctas", type=int, default=16,
+                    help="select/verify one-warp CTAs per SM in pipeline mode (leaves room for the commit CTA)")
     args = ap.parse_args()
+    args.pipeline_on = args.schedule == "pipeline"
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
 

@@ -321,11 +321,14 @@ class Pipeline:
     k overlapping the verification of batch k-1.
 
     Main stream: select(k), verify(k-1), select(k+1), verify(k), ...  Side stream:
-    commit(k) after select(k).  Two buffer sets alternate; select/verify run three
-    CTAs per SM and the commitment its co-resident form, so both kernels share every
-    SM.  Results are identical to the serial ``Plan`` calls."""
+    commit(k) after select(k).  Two buffer sets alternate.  select/verify run 16
+    one-warp CTAs per SM (16 x 32 x 96 registers) and the commitment its co-resident
+    form (8 warps, <= 64 registers, 64 KiB half inverse table), which together fill
+    the SM's 64 Ki registers exactly: the issue-bound commitment runs in the slots the
+    HBM-bound streaming kernels leave idle.  Results are identical to the serial
+    ``Plan`` calls."""
 
-    def __init__(self, eng: "ToplocEngine", row_offsets, H: int, ctas_per_sm: int = 3):
+    def __init__(self, eng: "ToplocEngine", row_offsets, H: int, ctas_per_sm: int = 16):
         self.plans = [Plan(eng, row_offsets, H), Plan(eng, row_offsets, H)]
         self.eng = eng
         self.ctas = ctas_per_sm
