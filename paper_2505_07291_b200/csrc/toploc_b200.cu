@@ -59,6 +59,10 @@ constexpr int kSpecSlots = 8192;              // speculation slots in the worksp
 #define TL_COMMIT_WARPS 32
 #endif
 constexpr int kCommitWarps = TL_COMMIT_WARPS;
+#ifndef TL_CO_COMMIT_WARPS
+#define TL_CO_COMMIT_WARPS 8  // co-resident commit CTA (pipeline): warps, <= 64 registers each
+#endif
+constexpr int kCoCommitWarps = TL_CO_COMMIT_WARPS;
 #ifndef TL_NDD_UNROLL
 #define TL_NDD_UNROLL 2  // divided-difference levels per loop iteration
 #endif
@@ -823,7 +827,7 @@ __device__ __forceinline__ void commit_chunk(const uint32_t (&raw)[4], const uin
 // (HALF = 64 KiB half table and <= 64 registers, so the CTA fits beside three
 // select/verify CTAs for the overlapped pipeline).
 template <int WARPS, bool HALF>
-__global__ void __launch_bounds__(WARPS * 32, HALF ? 4 : 1)
+__global__ void __launch_bounds__(WARPS * 32, HALF ? 1024 / (WARPS * 32) : 1)
 commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits, int64_t n_chunks,
               int K, const uint16_t* __restrict__ inv_tables, uint8_t* __restrict__ proofs,
               unsigned long long* __restrict__ next) {
@@ -1179,7 +1183,7 @@ int launch_commit_t(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, 
 // half table, <= 64 registers -- fits beside three select/verify CTAs per SM.
 int launch_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, const uint16_t* tables,
                   uint8_t* proofs, unsigned long long* next, int co_resident, cudaStream_t st) {
-  return co_resident ? launch_commit_t<8, true>(idx, bits, n_chunks, K, tables, proofs, next, st)
+  return co_resident ? launch_commit_t<kCoCommitWarps, true>(idx, bits, n_chunks, K, tables, proofs, next, st)
                      : launch_commit_t<kCommitWarps, false>(idx, bits, n_chunks, K, tables, proofs, next, st);
 }
 
