@@ -35,7 +35,8 @@ def round6_device(hidden, device=None) -> torch.Tensor:
         if t.dtype not in _DTYPE_CODE:
             t = t.to(torch.float64)
     else:
-        t = torch.from_numpy(np.ascontiguousarray(np.asarray(hidden, dtype=np.float64)))
+        a = np.ascontiguousarray(np.asarray(hidden, dtype=np.float64))
+        t = torch.from_numpy(a if a.flags.writeable else a.copy())  # torch wants a writable buffer
     t = t.to(dev, non_blocking=True).contiguous()
     out = torch.empty(t.shape, dtype=torch.float64, device=dev)
     lib = _ffi.load()
