@@ -1,0 +1,113 @@
+"""TOPLOC proofs on the rollout-file wire format.
+
+The reference carries one commitment per ``commit_interval`` output tokens as a hex
+string in ``RolloutRecord.commitments`` (``worker/files.py:37``), checks the count
+``ceil(T / commit_interval)`` (``files.py:184-186``) and trusts the header's interval
+(``validator/checks.py:211``).  A 258-byte TOPLOC proof is 516 hex characters in the
+same field with the same count, so the file schema does not change; TOPLOC mode
+additionally requires ``commit_interval == 32`` because proofs are defined over
+32-token chunks.
+
+``encode`` turns a proof batch into per-rollout hex lists; ``decode`` validates and
+packs per-rollout hex lists back into the (n_chunks, 258) uint8 layout ``tl_verify``
+reads.  Errors raise ``ProofFormatError`` (a ``ValueError``, like the reference's
+``RolloutSchemaError``) naming the rollout and item.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+TOPLOC_INTERVAL = 32
+PROOF_BYTES = 258
+PROOF_HEX = 2 * PROOF_BYTES
+_HEX = np.frombuffer(b"0123456789abcdef", dtype=np.uint8)
+
+
+class ProofFormatError(ValueError):
+    """A commitment list that cannot be a TOPLOC proof list."""
+
+
+def expected_count(n_tokens: int, interval: int = TOPLOC_INTERVAL) -> int:
+    """Commitments per record: ceil(T / interval) (``files.py:184-186``)."""
+    if interval < 1:
+        raise ValueError("interval must be >= 1")
+    return -(-int(n_tokens) // int(interval))
+
+
+def check_interval(commit_interval: int) -> None:
+    if int(commit_interval) != TOPLOC_INTERVAL:
+        raise ProofFormatError(f"commit_interval {commit_interval} != {TOPLOC_INTERVAL} (TOPLOC chunks)")
+
+
+def _as_array(proofs) -> np.ndarray:
+    if hasattr(proofs, "proofs"):  # api.ProofBatch
+        proofs = proofs.proofs
+    if hasattr(proofs, "detach"):  # torch tensor (device or host)
+        proofs = proofs.detach().cpu().numpy()
+    arr = np.ascontiguousarray(np.asarray(proofs, dtype=np.uint8))
+    if arr.ndim != 2 or arr.shape[1] != PROOF_BYTES:
+        raise ProofFormatError(f"proofs must be (n, {PROOF_BYTES}) bytes, got {arr.shape}")
+    return arr
+
+
+def encode(proofs, row_offsets=None, chunk_offsets=None) -> list[list[str]]:
+    """(n_chunks, 258) proofs -> per-rollout lists of 516-char lowercase hex strings.
+
+    ``chunk_offsets`` (or ``row_offsets``, converted with the 32-token rule) gives each
+    rollout's proof range; without either, one rollout holds every proof."""
+    if chunk_offsets is None and hasattr(proofs, "chunk_offsets"):
+        chunk_offsets = proofs.chunk_offsets
+    arr = _as_array(proofs)
+    if chunk_offsets is None:
+        if row_offsets is None:
+            chunk_offsets = [0, arr.shape[0]]
+        else:
+            lens = np.diff(np.asarray(row_offsets, dtype=np.int64))
+            chunk_offsets = np.concatenate([[0], np.cumsum(-(-lens // TOPLOC_INTERVAL))])
+    co = np.asarray(chunk_offsets, dtype=np.int64)
+    if co[0] != 0 or co[-1] != arr.shape[0] or np.any(np.diff(co) < 0):
+        raise ProofFormatError("chunk offsets do not tile the proofs")
+    # vectorised hex: two nibbles per byte through a 16-entry table
+    hexed = np.empty((arr.shape[0], PROOF_HEX), dtype=np.uint8)
+    hexed[:, 0::2] = _HEX[arr >> 4]
+    hexed[:, 1::2] = _HEX[arr & 15]
+    rows = [bytes(r).decode("ascii") for r in hexed]
+    return [rows[int(co[r]):int(co[r + 1])] for r in range(len(co) - 1)]
+
+
+def decode(commitments, n_tokens=None, interval: int = TOPLOC_INTERVAL) -> tuple[np.ndarray, np.ndarray]:
+    """Per-rollout hex lists -> ((n_chunks, 258) uint8, chunk offsets).
+
+    Checks each item is 516 hex characters and, when ``n_tokens`` (one per rollout)
+    is given, that every list has ``ceil(T / interval)`` items."""
+    check_interval(interval)
+    counts, blobs = [], []
+    for r, items in enumerate(commitments):
+        items = list(items)
+        if n_tokens is not None:
+            want = expected_count(n_tokens[r], interval)
+            if len(items) != want:
+                raise ProofFormatError(f"rollout {r}: {len(items)} commitments, expected {want}")
+        for i, s in enumerate(items):
+            if not isinstance(s, str) or len(s) != PROOF_HEX:
+                raise ProofFormatError(f"rollout {r} item {i}: not a {PROOF_HEX}-char proof")
+            try:
+                blobs.append(bytes.fromhex(s))
+            except ValueError:
+                raise ProofFormatError(f"rollout {r} item {i}: not hex") from None
+        counts.append(len(items))
+    arr = np.frombuffer(b"".join(blobs), dtype=np.uint8).reshape(-1, PROOF_BYTES).copy() if blobs else \
+        np.zeros((0, PROOF_BYTES), dtype=np.uint8)
+    return arr, np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+
+
+def modulus(proof_hex_or_bytes) -> int:
+    """The proof's modulus field (big-endian u16): a prime in [32771, 65497], or 0 for an
+    unprovable chunk."""
+    b = bytes.fromhex(proof_hex_or_bytes) if isinstance(proof_hex_or_bytes, str) else bytes(proof_hex_or_bytes)
+    return int.from_bytes(b[:2], "big")
+
+
+__all__ = ["ProofFormatError", "TOPLOC_INTERVAL", "PROOF_BYTES", "PROOF_HEX", "expected_count", "check_interval",
+           "encode", "decode", "modulus"]

@@ -27,12 +27,13 @@ equality then holds) or an empty list when they fail (reject("commitment")).
 from __future__ import annotations
 
 import contextvars
-import math
 from dataclasses import dataclass
 
 import numpy as np
 
-TOPLOC_CHUNK = 32
+from . import codec
+
+TOPLOC_CHUNK = codec.TOPLOC_INTERVAL
 _SITES = ("swarm.worker.rollout", "swarm.worker", "swarm.validator.checks", "swarm.validator.adversaries")
 _saved: dict = {}
 _claimed: contextvars.ContextVar = contextvars.ContextVar("toploc_claimed", default=None)
@@ -106,13 +107,11 @@ def install(mode: str = "exact", thresholds=None, backend=None) -> None:
         if queue is None:   # called outside validate_file: behave like the prover
             return prove_commitments(hidden, k)
         claimed = queue.pop(0)
-        try:
-            proofs = [bytes.fromhex(h) for h in claimed]
-        except (ValueError, TypeError):
+        try:  # 516-char hex items, ceil(T / 32) of them (codec.py, files.py:184-186)
+            arr, _ = codec.decode([claimed], n_tokens=[len(hidden)], interval=k)
+        except codec.ProofFormatError:
             return []
-        T = len(hidden)
-        if len(proofs) != math.ceil(T / k) or any(len(p) != 258 for p in proofs):
-            return []
+        proofs = [arr[j].tobytes() for j in range(arr.shape[0])]
         return proofs if backend.verify(to_bf16_bits(hidden), proofs, k, th) else []
 
     orig_validate = _saved[("swarm.validator.checks", "validate_file")]
@@ -125,12 +124,14 @@ def install(mode: str = "exact", thresholds=None, backend=None) -> None:
             queue = [list(f.records[i].commitments) for i in sorted(_commit_sample(f, ctx))]
         except (RolloutSchemaError, Exception):
             f, queue = None, []
-        if f is not None and f.commit_interval != TOPLOC_CHUNK:
+        if f is not None:
             # TOPLOC proofs are defined over 32-token chunks; the reference trusts the
             # header's interval (checks.py:211), TOPLOC mode enforces it
-            return Verdict(file_id=f.file_id, result="reject", failed_check="schema",
-                           details=f"commit_interval {f.commit_interval} != {TOPLOC_CHUNK}",
-                           node_address=f.node_address, step=f.step)
+            try:
+                codec.check_interval(f.commit_interval)
+            except codec.ProofFormatError as e:
+                return Verdict(file_id=f.file_id, result="reject", failed_check="schema", details=str(e),
+                               node_address=f.node_address, step=f.step)
         token = _claimed.set(queue)
         try:
             return orig_validate(data, ctx, expected_identity)
