@@ -106,11 +106,12 @@ int tl_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_
               uint8_t* proofs_out, void* workspace, size_t workspace_bytes, void* stream);
 
 /*
- * Launch-shape variants for pipelining a stream of batches (prove of batch k+1
- * overlapping verify of batch k on a second stream).  ctas_per_sm caps the
- * persistent select/verify grid (0 = occupancy maximum, 4); co_resident = 1 runs
- * the commitment with 8 warps and a 64 KiB half inverse table so one commit CTA
- * fits on an SM beside three select/verify CTAs.  Results are identical.
+ * Launch-shape variants for pipelining a stream of batches (the commitment of
+ * batch k on a second stream, beside verify of batch k-1 and select of k+1).
+ * ctas_per_sm caps the persistent select/verify grid of one-warp CTAs (0 = the
+ * occupancy maximum, 18 per SM; 16 leaves the registers for one commit CTA);
+ * co_resident = 1 runs the commitment with 8 warps (<= 64 registers) and a 64 KiB
+ * half inverse table so that CTA fits beside them.  Results are identical.
  */
 int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
                  int32_t H, int32_t C, int32_t K, int64_t n_chunks, int32_t* idx_out,
@@ -138,6 +139,37 @@ int tl_verify(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, in
               const tl_thresholds* thresholds_host, tl_chunk_stats* stats_out,
               uint8_t* chunk_accept_out, uint8_t* rollout_accept_out, void* workspace,
               size_t workspace_bytes, void* stream);
+
+/*
+ * Per-record checks that share the validator's prefill, in the
+ * reference's order (checks.py:204-213): termination (checks.py:120-131), then
+ * sampling (checks.py:134-142), then the commitment verdict.
+ *   probs         : float64 chosen-token probabilities, rollouts concatenated,
+ *                   delimited by row_off (device int64 [n_roll + 1]);
+ *   prompt_len    : device int32 [n_roll]; ends_with_eos: device uint8 [n_roll]
+ *                   (output[-1] == eos_id);
+ *   commit_accept : nullable device uint8 [n_roll], e.g. tl_verify's rollout verdicts;
+ *   commit_checked: nullable device uint8 [n_roll], 1 = in the commitment sample
+ *                   (checks.py:145-151); NULL = every record is checked;
+ *   verdict_out   : device int32 [n_roll]: 0 accept, 1 termination, 2 sampling,
+ *                   3 commitment (first failing check);
+ *   frac_out, p_last_out: nullable device float64 [n_roll]: fraction of probs
+ *                   below p_low (exact count / T), probs[T-1] (NaN when T = 0).
+ * A record with T = 0 fails termination unless prompt_len >= max_len.
+ */
+typedef struct tl_record_thresholds {
+  int32_t max_len;           /* ModelConfig.max_len                       */
+  int32_t min_sampling_len;  /* CheckContext.min_sampling_len (16)         */
+  double eos_prob_floor;     /* CheckContext.eos_prob_floor (0.1)          */
+  double p_low;              /* CheckContext.p_low (0.005)                 */
+  double theta;              /* CheckContext.theta (0.25)                  */
+} tl_record_thresholds;
+
+int tl_record_checks(const double* probs, const int64_t* row_off, int32_t n_roll,
+                     const int32_t* prompt_len, const uint8_t* ends_with_eos,
+                     const tl_record_thresholds* thresholds_host, const uint8_t* commit_accept,
+                     const uint8_t* commit_checked, int32_t* verdict_out, double* frac_out,
+                     double* p_last_out, void* stream);
 
 /*
  * Exact mode (reference parity shim for build_commitments, rollout.py:65):

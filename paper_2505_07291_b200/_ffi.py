@@ -31,6 +31,11 @@ class ChunkStats(ctypes.Structure):
                 ("mant_mean", ctypes.c_double), ("mant_median", ctypes.c_double)]
 
 
+class RecordThresholds(ctypes.Structure):
+    _fields_ = [("max_len", ctypes.c_int32), ("min_sampling_len", ctypes.c_int32),
+                ("eos_prob_floor", ctypes.c_double), ("p_low", ctypes.c_double), ("theta", ctypes.c_double)]
+
+
 # name -> (restype, argtypes); must match include/toploc_b200.h
 SYMBOLS = {
     "tl_strerror": (ctypes.c_char_p, [c_i32]),
@@ -49,6 +54,7 @@ SYMBOLS = {
     "tl_verify": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_i64, c_vp,
                           ctypes.POINTER(Thresholds), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "tl_round6": (c_i32, [c_vp, c_i32, c_i64, c_vp, c_vp]),
+    "tl_record_checks": (c_i32, [c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tl_synth_bf16": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_u64, c_i32, c_vp, c_vp, c_i32, c_u64, c_vp]),
 }
 

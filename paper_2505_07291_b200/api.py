@@ -50,6 +50,26 @@ class Thresholds:
                                float(self.max_mant_median))
 
 
+@dataclass(frozen=True)
+class RecordThresholds:
+    """The prefill-sharing record checks' parameters: ``ModelConfig.max_len`` and
+    ``CheckContext`` (swarm/validator/checks.py:62-65) with the reference's defaults."""
+
+    max_len: int
+    min_sampling_len: int = 16
+    eos_prob_floor: float = 0.1
+    p_low: float = 0.005
+    theta: float = 0.25
+
+    def to_c(self) -> _ffi.RecordThresholds:
+        return _ffi.RecordThresholds(int(self.max_len), int(self.min_sampling_len), float(self.eos_prob_floor),
+                                     float(self.p_low), float(self.theta))
+
+
+# verdict codes of record_checks / tl_record_checks (the reference's failed_check names)
+RECORD_VERDICTS = ("accept", "termination", "sampling", "commitment")
+
+
 @dataclass
 class VerificationResult:
     """Per-chunk result (field names follow upstream toploc's VerificationResult)."""
@@ -395,6 +415,40 @@ def verify_proofs(hidden, row_offsets, proofs, chunk: int = CHUNK, topk: int = T
     eng = engine(device, chunk, topk)
     vb = eng.verify(hidden, row_offsets, proofs, thresholds)
     return vb.results(), [bool(v) for v in vb.rollout_accept.cpu().tolist()]
+
+
+def record_checks(probs, row_offsets, prompt_len, ends_with_eos, thresholds: RecordThresholds,
+                  commit_accept=None, commit_checked=None, device=None):
+    """tl_record_checks: the validator's per-record termination and sampling checks on
+    the prefill's chosen-token probabilities, then the commitment verdict, in the
+    reference's order (checks.py:204-213).  ``probs``: float64 per output token,
+    rollouts concatenated by ``row_offsets``; ``commit_accept`` e.g. a VerifyBatch's
+    ``rollout_accept``.  Returns device tensors (verdict int32 codes indexing
+    RECORD_VERDICTS, fraction of probs below p_low, last-token prob)."""
+    _require_cuda()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    p = torch.as_tensor(probs, dtype=torch.float64).reshape(-1).to(dev).contiguous()
+    offs = normalize_offsets(row_offsets, p.numel())
+    R = len(offs) - 1
+    offs_dev = torch.from_numpy(offs).to(dev)
+
+    def vec(x, dtype):
+        t = None if x is None else torch.as_tensor(x).reshape(-1).to(dev, dtype).contiguous()
+        if t is not None and t.numel() != R:
+            raise ValueError(f"per-record arrays need {R} entries, got {t.numel()}")
+        return t
+
+    pl, eos = vec(prompt_len, torch.int32), vec(ends_with_eos, torch.uint8)
+    ca, cc = vec(commit_accept, torch.uint8), vec(commit_checked, torch.uint8)
+    verdict = torch.empty(R, dtype=torch.int32, device=dev)
+    frac = torch.empty(R, dtype=torch.float64, device=dev)
+    p_last = torch.empty(R, dtype=torch.float64, device=dev)
+    th = thresholds.to_c()
+    rc = _ffi.load().tl_record_checks(p.data_ptr(), offs_dev.data_ptr(), R, _ptr(pl), _ptr(eos), ctypes.byref(th),
+                                      _ptr(ca), _ptr(cc), verdict.data_ptr(), frac.data_ptr(), p_last.data_ptr(),
+                                      _stream_handle(dev))
+    _ffi.check(rc, "tl_record_checks")
+    return verdict, frac, p_last
 
 
 def build_commitments(hidden, k: int = CHUNK) -> list[bytes]:

@@ -1027,6 +1027,37 @@ __global__ void rollout_verdict_kernel(const uint8_t* __restrict__ chunk_accept,
   if (lane == 0) out[r] = (uint8_t)ok;
 }
 
+// ----------------------------------------------------------------------------- record checks
+// One warp per record: termination (checks.py:120-131), sampling (checks.py:134-142),
+// commitment verdict, in the reference's order.  The sampling fraction is the exact
+// count of probs < p_low divided once in float64, like np.mean over a bool array.
+__global__ void record_checks_kernel(const double* __restrict__ probs, const int64_t* __restrict__ row_off,
+                                     int n_roll, const int32_t* __restrict__ prompt_len,
+                                     const uint8_t* __restrict__ ends_with_eos, tl_record_thresholds th,
+                                     const uint8_t* __restrict__ commit_accept,
+                                     const uint8_t* __restrict__ commit_checked, int32_t* __restrict__ verdict_out,
+                                     double* __restrict__ frac_out, double* __restrict__ p_last_out) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n_roll) return;
+  const int64_t lo = row_off[r], T = row_off[r + 1] - lo;
+  unsigned long long cnt = 0;
+  for (int64_t i = lane; i < T; i += 32) cnt += probs[lo + i] < th.p_low ? 1ull : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+  if (lane != 0) return;
+  const double frac = T > 0 ? __ddiv_rn((double)cnt, (double)T) : 0.0;
+  const double p_last = T > 0 ? probs[lo + T - 1] : __longlong_as_double(0x7FF8000000000000ll);
+  const bool term_ok = (int64_t)prompt_len[r] + T >= (int64_t)th.max_len ||
+                       (T > 0 && ends_with_eos[r] && p_last > th.eos_prob_floor);
+  const bool samp_ok = T < (int64_t)th.min_sampling_len || !(frac > th.theta);
+  const bool checked = commit_checked == nullptr || commit_checked[r] != 0;
+  const bool com_ok = commit_accept == nullptr || !checked || commit_accept[r] != 0;
+  verdict_out[r] = !term_ok ? 1 : !samp_ok ? 2 : !com_ok ? 3 : 0;
+  if (frac_out) frac_out[r] = frac;
+  if (p_last_out) p_last_out[r] = p_last;
+}
+
 // ----------------------------------------------------------------------------- exact mode
 __device__ __forceinline__ double load_as_f64(const void* in, int dtype, int64_t i) {
   switch (dtype) {
@@ -1346,6 +1377,19 @@ int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   }
   if (rollout_accept_out)
     rollout_verdict_kernel<<<(n_roll + 7) / 8, 256, 0, st>>>(accept, prefix, n_roll, rollout_accept_out);
+  return launch_status();
+}
+
+int tl_record_checks(const double* probs, const int64_t* row_off, int32_t n_roll, const int32_t* prompt_len,
+                     const uint8_t* ends_with_eos, const tl_record_thresholds* thresholds_host,
+                     const uint8_t* commit_accept, const uint8_t* commit_checked, int32_t* verdict_out,
+                     double* frac_out, double* p_last_out, void* stream) {
+  if (n_roll < 0 || !thresholds_host) return TL_EINVAL;
+  if (n_roll == 0) return TL_OK;
+  if (!probs || !row_off || !prompt_len || !ends_with_eos || !verdict_out) return TL_EINVAL;
+  record_checks_kernel<<<(n_roll + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      probs, row_off, n_roll, prompt_len, ends_with_eos, *thresholds_host, commit_accept, commit_checked,
+      verdict_out, frac_out, p_last_out);
   return launch_status();
 }
 

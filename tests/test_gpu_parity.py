@@ -341,3 +341,34 @@ def test_prove_verify_other_chunk_and_topk(K, C, H, offs):
     jit = synth_bits(0, offs[-1], H, K + C, 1, jitter_thr=6000, jitter_seed=3)
     for th in (api.Thresholds(), api.Thresholds(0, 0.0, 0.0)):
         check_verify_against_oracle(jit, offs, pf, th, K=K, C=C)
+
+
+# ----------------------------------------------------------------------------- record checks
+def test_record_checks_match_oracle():
+    """tl_record_checks (termination, sampling, commitment in the reference's order,
+    checks.py:204-213) against oracle/checks_oracle.py, boundaries included."""
+    from oracle import checks_oracle as CO
+    rng = np.random.default_rng(11)
+    probs, prompt, eos = [], [], []
+    for i in range(500):
+        T = int(rng.integers(0, 80)) if i else 0
+        p = rng.choice([0.005, 0.0049999999, 0.1, 0.10000001, 0.5, 1e-4, 0.9], size=T) if i % 3 == 0 \
+            else rng.random(T) ** 3
+        probs.append(p)
+        prompt.append(int(rng.integers(1, 40)))
+        eos.append(int(rng.integers(0, 2)))
+    probs += [np.array([0.001] * 4 + [0.5] * 12), np.array([0.001] * 5 + [0.5] * 11), np.array([0.5] * 15 + [0.1])]
+    prompt += [1, 1, 1]
+    eos += [1, 1, 1]
+    R = len(probs)
+    acc = rng.integers(0, 2, size=R)
+    chk = rng.integers(0, 2, size=R)
+    offs = np.concatenate([[0], np.cumsum([len(p) for p in probs])])
+    th = api.RecordThresholds(max_len=64)
+    verdict, frac, p_last = api.record_checks(np.concatenate(probs), offs, prompt, eos, th, acc, chk)
+    want = CO.record_verdicts(probs, prompt, eos, 64, commit_accept=acc, commit_checked=chk)
+    v, f, pl = verdict.cpu().numpy(), frac.cpu().numpy(), p_last.cpu().numpy()
+    assert [int(x) for x in v] == [w[0] for w in want]
+    assert np.array_equal(f, np.array([w[1] for w in want]))   # exact count / T, like np.mean
+    for r in range(R):
+        assert (np.isnan(pl[r]) and len(probs[r]) == 0) or pl[r] == probs[r][-1]
