@@ -824,8 +824,8 @@ __device__ __forceinline__ void commit_chunk(const uint32_t (&raw)[4], const uin
 
 // tl_commit: one warp per chunk over (idx, bits) in global memory.  WARPS x 32
 // threads, one CTA per SM, the first prime's inverse table staged in shared memory
-// (HALF = 64 KiB half table and <= 64 registers, so the CTA fits beside three
-// select/verify CTAs for the overlapped pipeline).
+// (HALF = 64 KiB half table and <= 64 registers, so the CTA fits beside 16 one-warp
+// select/verify CTAs for the overlapped pipeline, api.Pipeline).
 template <int WARPS, bool HALF>
 __global__ void __launch_bounds__(WARPS * 32, HALF ? 1024 / (WARPS * 32) : 1)
 commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits, int64_t n_chunks,
@@ -1210,8 +1210,8 @@ int launch_commit_t(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, 
   return launch_status();
 }
 
-// co_resident = 0: 16 warps, full 128 KiB table (fastest alone); 1: 8 warps, 64 KiB
-// half table, <= 64 registers -- fits beside three select/verify CTAs per SM.
+// co_resident = 0: 32 warps, full 128 KiB table (fastest alone); 1: 8 warps, 64 KiB
+// half table, <= 64 registers -- fits beside 16 one-warp select/verify CTAs per SM.
 int launch_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, const uint16_t* tables,
                   uint8_t* proofs, unsigned long long* next, int co_resident, cudaStream_t st) {
   return co_resident ? launch_commit_t<kCoCommitWarps, true>(idx, bits, n_chunks, K, tables, proofs, next, st)
