@@ -19,7 +19,11 @@
  *     NULL = legacy default stream); no host synchronisation inside;
  *   - return 0 on success or a negative TL_E* code; tl_strerror() names it;
  *   - the library keeps no mutable global state (safe from many host threads,
- *     one stream per thread / device).
+ *     one stream per thread / device);
+ *   - a workspace (tl_workspace_bytes) serves one call at a time: calls that may
+ *     run concurrently need their own.  Between calls it carries the select
+ *     kernels' threshold speculation, which only steers speed (any content,
+ *     including uninitialised memory, gives the same results).
  *
  * Layout
  *   hidden   : bf16 bit patterns, row-major (n_rows, H), rollouts concatenated

@@ -212,8 +212,10 @@ __device__ __forceinline__ Spec spec_load(const uint4* slots, int64_t gw) {
   }
   return sp;
 }
+// A warp that selected no chunk this launch (k1 still the initial 0x7FFF) leaves its
+// slot alone: storing the untrained state would start a later launch far too high.
 __device__ __forceinline__ void spec_store(uint4* slots, int64_t gw, const Spec& sp, int lane) {
-  if (lane == 0 && sp.k1 <= 0x7FFFu)
+  if (lane == 0 && sp.k1 < 0x7FFFu)
     slots[gw % kSpecSlots] = make_uint4(sp.k0, sp.k1, (unsigned)sp.delta, kSpecMagic);
 }
 
