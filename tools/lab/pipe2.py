@@ -19,12 +19,12 @@ eng = api.engine()
 
 
 class Pipe3:
-    def __init__(self, ctas=16):
+    def __init__(self, ctas=16, side_prio=0):
         self.plans = [api.Plan(eng, offs, H), api.Plan(eng, offs, H)]
         for p in self.plans:  # verify gets its own workspace (prefix, chunk counter, speculation)
             p.ws_v = torch.empty_like(p.ws)
         self.ctas = ctas
-        self.side = torch.cuda.Stream()
+        self.side = torch.cuda.Stream(priority=side_prio)
         self.vs = torch.cuda.Stream()
 
     def verify(self, pl, h, stream):
@@ -81,10 +81,15 @@ def timeit(fn, n):
 
 
 p2 = api.Pipeline(eng, offs, H)
-ms2, r2 = timeit(lambda n: p2.run([prv] * n, [val] * n), steps)
-print(f"api.Pipeline: {ms2:.3f} ms/step  {R * T / ms2 / 1e3:.1f} M tok/s")
-for c in (16, 14, 12):
-    p3 = Pipe3(c)
-    ms3, r3 = timeit(p3.run, steps)
-    ok = all(torch.equal(a, r2[0]) for a in r3)
-    print(f"3-stream ctas {c}: {ms3:.3f} ms/step  {R * T / ms3 / 1e3:.1f} M tok/s  verdicts equal {ok}")
+p2h = api.Pipeline(eng, offs, H)
+p2h.side = torch.cuda.Stream(priority=-1)
+p3 = Pipe3(16, -1)
+ref = None
+for rep in range(2):
+    for name, fn in (("api.Pipeline prio 0", lambda n: p2.run([prv] * n, [val] * n)),
+                     ("api.Pipeline prio -1", lambda n: p2h.run([prv] * n, [val] * n)),
+                     ("3-stream prio -1", p3.run)):
+        ms, r = timeit(fn, steps)
+        ref = r[0] if ref is None else ref
+        ok = all(torch.equal(a, ref) for a in r)
+        print(f"{name}: {ms:.3f} ms/step  {R * T / ms / 1e3:.1f} M tok/s  verdicts equal {ok}", flush=True)
