@@ -255,6 +255,11 @@ def run_b200(args, cfg, rank, world, local_rank):
         spot = {"chunks": js, "proofs_bit_exact": all(okp)}
 
     pipe = api.Pipeline(eng, offs, H, ctas_per_sm=args.ctas) if args.pipeline_on else None
+    graph = api.StepGraph(plan, prv, val) if args.schedule == "graph" else None
+    if graph is not None:
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize(dev)
     if pipe is not None:
         pipe.run([prv] * args.warmup, [val] * args.warmup)
         torch.cuda.synchronize(dev)
@@ -286,6 +291,14 @@ def run_b200(args, cfg, rank, world, local_rank):
         spot_pipe = bool(torch.equal(pipe.plans[(args.steps - 1) % 2].proofs, plan.proofs))
         if spot is not None:
             spot["pipeline_proofs_equal_serial"] = spot_pipe
+    elif args.schedule == "graph":
+        t_start.record(stream)
+        for k in range(args.steps):
+            graph.replay()
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+        sel_ms, com_ms, ver_ms = serial_ms["select"], serial_ms["commit"], serial_ms["verify"]
+        accepted = int(plan.rollout_accept.sum().item())
     else:
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
         t_start.record(stream)
@@ -406,7 +419,9 @@ def run_b200(args, cfg, rank, world, local_rank):
                           "verify_gbs": ver_bytes / (ver_ms / 1e3) / 1e9, "verdict_gather": gather_ms,
                           "serial": serial_ms,
                           "schedule": (f"pipelined: commit(k) on a side stream overlaps verify(k-1); "
-                                       f"select/verify {args.ctas} CTAs/SM" if args.pipeline_on else "serial")},
+                                       f"select/verify {args.ctas} CTAs/SM" if args.pipeline_on else
+                                       "graph: serial step replayed as one CUDA graph" if args.schedule == "graph"
+                                       else "serial")},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
@@ -431,9 +446,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-tokens", type=int, default=8192)
     ap.add_argument("--no-spot-check", dest="spot_check", action="store_false")
-    ap.add_argument("--schedule", default="pipeline", choices=["pipeline", "serial"],
+    ap.add_argument("--schedule", default="pipeline", choices=["pipeline", "serial", "graph"],
                     help="pipeline (default): commit(k) on a side stream overlaps verify(k-1) and select(k+1); "
-                         "serial: tl_select, tl_commit, tl_verify back to back")
+                         "serial: tl_select, tl_commit, tl_verify back to back; graph: the serial step "
+                         "captured as one CUDA graph (api.StepGraph) and replayed")
     ap.add_argument("--pipeline", dest="schedule", action="store_const", const="pipeline")
     ap.add_argument("--serial", dest="schedule", action="store_const", const="serial")
     ap.add_argument("--ctas", type=int, default=16,

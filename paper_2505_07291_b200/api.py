@@ -336,6 +336,36 @@ class Plan:
         return self.rollout_accept
 
 
+class StepGraph:
+    """One prove + verify step of a ``Plan`` captured as a CUDA graph (select, commit,
+    verify and their small kernels: 7 launches replayed as one).  The captured tensors
+    are the ones given at capture time; refill them in place between replays.  Launch
+    overhead matters for small batches (configuration 1 is launch-bound); results are
+    identical to the eager calls."""
+
+    def __init__(self, plan: "Plan", prover: torch.Tensor, validator: torch.Tensor,
+                 thresholds: Thresholds = Thresholds()):
+        self.plan = plan
+        dev = plan.eng.device
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # warm the kernels' attributes outside the capture
+            plan.select(prover)
+            plan.commit()
+            plan.verify(validator, None, thresholds)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            plan.select(prover)
+            plan.commit()
+            plan.verify(validator, None, thresholds)
+
+    def replay(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.plan.rollout_accept
+
+
 class Pipeline:
     """Prove + verify a stream of equally-shaped batches with the commitment of batch
     k overlapping the verification of batch k-1.

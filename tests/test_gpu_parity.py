@@ -372,3 +372,28 @@ def test_record_checks_match_oracle():
     assert np.array_equal(f, np.array([w[1] for w in want]))   # exact count / T, like np.mean
     for r in range(R):
         assert (np.isnan(pl[r]) and len(probs[r]) == 0) or pl[r] == probs[r][-1]
+
+
+def test_step_graph_matches_eager():
+    """A Plan's prove + verify captured as one CUDA graph replays to the eager results."""
+    H, offs = 1024, [0, 70, 128, 2048]
+    bits = synth_bits(0, offs[-1], H, seed=4, dist=1)
+    jit = synth_bits(0, offs[-1], H, seed=4, dist=1, jitter_thr=3277, jitter_seed=5)
+    prv = torch.from_numpy(bits.view(np.int16)).cuda()
+    val = torch.from_numpy(jit.view(np.int16)).cuda()
+    plan = api.engine().plan(offs, H)
+    plan.select(prv)
+    plan.commit()
+    plan.verify(val)
+    torch.cuda.synchronize()
+    want_p, want_s, want_a = plan.proofs.clone(), plan.stats.clone(), plan.rollout_accept.clone()
+    g = api.StepGraph(plan, prv, val)
+    for _ in range(3):
+        plan.proofs.zero_()
+        plan.stats.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(plan.proofs, want_p) and torch.equal(plan.stats, want_s)
+        assert torch.equal(plan.rollout_accept, want_a)
+    _, _, proofs = TO.prove_chunks(TO._chunks_of(bits, offs, 32)[1], 128)
+    assert all(plan.proofs[j].cpu().numpy().tobytes() == proofs[j] for j in range(len(proofs)))
