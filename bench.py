@@ -204,11 +204,22 @@ def run_b200(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     R, T, H = cfg["R"], cfg["T"], cfg["H"]
-    n_rows = R * T
+    R_total = R
     d = DISTS[args.dist]
-    seed = 1000 + rank
-    prv = synth_device(n_rows, H, seed, d, device=dev)
-    val = synth_device(n_rows, H, seed, d, jitter_thr=JITTER_THR, jitter_seed=seed + 1, device=dev)
+    shard = None
+    if args.scaling == "strong":
+        # the configuration's rollouts are one job sharded over the ranks by token count
+        # (scheduler.shard_by_tokens); every rank generates its slice of the same tensor
+        from paper_2505_07291_b200 import scheduler
+        shard = scheduler.plan(np.full(R_total, T, dtype=np.int64), rank, world)
+        R, row0, seed = shard.hi - shard.lo, shard.lo * T, 1000
+        if R < 1:
+            raise SystemExit(f"rank {rank}: no rollouts to shard ({R_total} rollouts over {world} ranks)")
+    else:
+        row0, seed = 0, 1000 + rank
+    n_rows = R * T
+    prv = synth_device(n_rows, H, seed, d, row0=row0, device=dev)
+    val = synth_device(n_rows, H, seed, d, row0=row0, jitter_thr=JITTER_THR, jitter_seed=seed + 1, device=dev)
     offs = np.arange(R + 1, dtype=np.int64) * T
     eng = api.engine(dev)
     plan = eng.plan(offs, H)
@@ -325,16 +336,27 @@ def run_b200(args, cfg, rank, world, local_rank):
     gather_ms = None
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+
+        def gather():
+            if shard is not None:
+                from paper_2505_07291_b200 import scheduler
+                return scheduler.gather_verdicts(plan.rollout_accept, shard.counts())
+            out = torch.empty(world * R, dtype=torch.uint8, device=dev)
+            dist.all_gather_into_tensor(out, plan.rollout_accept)
+            return out
+
+        gather()  # first call sets up the collective's buffers; time the second
+        dist.barrier()
+        torch.cuda.synchronize(dev)
         g0 = torch.cuda.Event(enable_timing=True)
         g1 = torch.cuda.Event(enable_timing=True)
-        out = torch.empty(world * R, dtype=torch.uint8, device=dev)
         g0.record(stream)
-        dist.all_gather_into_tensor(out, plan.rollout_accept)
+        gather()
         g1.record(stream)
         torch.cuda.synchronize(dev)
         gather_ms = g0.elapsed_time(g1)
     max_ms = float(t.item())
-    tokens = world * R * T * args.steps
+    tokens = (R_total if shard is not None else world * R) * T * args.steps
     value = tokens / (max_ms / 1e3)
     ms_per_step = max_ms / args.steps
 
@@ -400,9 +422,10 @@ def run_b200(args, cfg, rank, world, local_rank):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u16", "data": "synthetic",
-            "config": {"workload": cfg["name"], "config": args.config, "rollouts_per_gpu": R, "tokens_per_rollout": T,
+            "config": {"workload": cfg["name"], "config": args.config, "rollouts_per_gpu": R,
+                       "rollouts_total": R_total if shard is not None else world * R, "tokens_per_rollout": T,
                        "hidden": H, "chunk": CHUNK, "topk": TOPK, "dist": args.dist,
                        "validator": "same states with 5% of elements +-1 ulp (GPU nondeterminism model)",
                        "l2": f"inputs {2 * n_rows * H * 2 / 1e9:.1f} GB per GPU >> 126 MB L2; no flush needed",
@@ -452,6 +475,9 @@ def main():
                          "captured as one CUDA graph (api.StepGraph) and replayed")
     ap.add_argument("--pipeline", dest="schedule", action="store_const", const="pipeline")
     ap.add_argument("--serial", dest="schedule", action="store_const", const="serial")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak (default): every rank runs the configuration; strong: the configuration's "
+                         "rollouts are sharded over the ranks by token count (scheduler.plan)")
     ap.add_argument("--ctas", type=int, default=16,
                     help="select/verify one-warp CTAs per SM in pipeline mode (leaves room for the commit CTA)")
     args = ap.parse_args()
