@@ -80,9 +80,15 @@ def build_commitments(hidden, k: int = 32) -> list[bytes]:
 _STAGING: dict = {}
 
 
+def release_staging() -> None:
+    """Free the cached device and pinned host staging of ``build_commitments_batch``
+    (2 x group_rows x H float64 each, 2.7 GB per buffer at the defaults and H = 5120)."""
+    _STAGING.clear()
+
+
 def _staging(dev, elems: int):
     """Double-buffered device + pinned host float64 staging, reused across calls
-    (pinning gigabytes per call would dominate)."""
+    (pinning gigabytes per call would dominate); ``release_staging`` frees it."""
     key = dev.index
     cur = _STAGING.get(key)
     if cur is None or cur[0][0].numel() < elems:
