@@ -397,3 +397,27 @@ def test_step_graph_matches_eager():
         assert torch.equal(plan.rollout_accept, want_a)
     _, _, proofs = TO.prove_chunks(TO._chunks_of(bits, offs, 32)[1], 128)
     assert all(plan.proofs[j].cpu().numpy().tobytes() == proofs[j] for j in range(len(proofs)))
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_fuzz_prove_verify_small_shapes(case):
+    """Seeded random shapes against the oracle: odd H (unaligned chunk starts), ragged and
+    empty rollouts, chunks smaller than K, K and C away from the defaults, all value
+    distributions and a jittered validator."""
+    rng = np.random.default_rng(1000 + case)
+    H = int(rng.choice([1, 3, 7, 17, 64, 129, 640, 1031]))
+    C = int(rng.choice([1, 4, 32, 32, 32, 33]))
+    K = int(rng.choice([1, 5, 64, 128, 128]))
+    if C * H >= (1 << 24) - 1:
+        C = 4
+    lens = rng.integers(0, 3 * C + 2, size=int(rng.integers(1, 6)))
+    offs = [0] + np.cumsum(lens).tolist()
+    if offs[-1] == 0:
+        offs[-1] = 1
+    dist = int(rng.integers(0, 4))
+    bits = synth_bits(0, offs[-1], H, seed=case, dist=dist)
+    check_prove_against_oracle(bits, offs, K=K, C=C)
+    pf = [bytes(b) for b in gpu_prove(bits, offs, K, C).proofs.cpu().numpy()]
+    jit = synth_bits(0, offs[-1], H, seed=case, dist=dist, jitter_thr=int(rng.integers(0, 20000)),
+                     jitter_seed=case + 7)
+    check_verify_against_oracle(jit, offs, pf, K=K, C=C)
