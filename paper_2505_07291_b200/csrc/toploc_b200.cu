@@ -147,8 +147,8 @@ __device__ __forceinline__ ChunkRef locate_chunk(const int64_t* __restrict__ pre
 
 // ----------------------------------------------------------------------------- streaming select
 //
-// One WARP owns one chunk at a time (persistent over chunks j = its global warp
-// id, + the total warp count, ...).  It streams the chunk's 16-byte vectors
+// One WARP owns one chunk at a time (persistent: first the chunk at its global warp
+// id, then chunks claimed from a counter, claim_chunk).  It streams the chunk's 16-byte vectors
 // (vector g of warp tile t: t*kWTileVec + u*32 + lane) through a register double
 // buffer of non-allocating loads.  Per lane and tile a bf16x2 |max| tree folds the
 // 8 U elements into one 16x2 maximum, tested with one add-and-mask against the
