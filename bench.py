@@ -265,7 +265,15 @@ def run_b200(args, cfg, rank, world, local_rank):
             okp.append(pr[0] == got[j].tobytes())
         spot = {"chunks": js, "proofs_bit_exact": all(okp)}
 
-    pipe = api.Pipeline(eng, offs, H, ctas_per_sm=args.ctas) if args.pipeline_on else None
+    pipe = None
+    if args.schedule == "partition":
+        try:
+            pipe = api.PartitionedPipeline(eng, offs, H, commit_sms=args.commit_sms)
+        except (RuntimeError, ValueError) as e:  # no green contexts: the co-resident pipeline instead
+            print(f"bench: SM partition unavailable ({e}); using --schedule pipeline", file=sys.stderr)
+            args.schedule = "pipeline"
+    if pipe is None:
+        pipe = api.Pipeline(eng, offs, H, ctas_per_sm=args.ctas) if args.pipeline_on else None
     graph = api.StepGraph(plan, prv, val) if args.schedule == "graph" else None
     if graph is not None:
         for _ in range(args.warmup):
@@ -441,7 +449,9 @@ def run_b200(args, cfg, rank, world, local_rank):
             "phases_ms": {"select": sel_ms, "commit": com_ms, "verify": ver_ms,
                           "verify_gbs": ver_bytes / (ver_ms / 1e3) / 1e9, "verdict_gather": gather_ms,
                           "serial": serial_ms,
-                          "schedule": (f"pipelined: commit(k) on a side stream overlaps verify(k-1); "
+                          "schedule": (f"partitioned: commit on {pipe.sms[1]} SMs, select/verify on {pipe.sms[0]} SMs "
+                                       f"(green contexts)" if args.schedule == "partition" else
+                                       f"pipelined: commit(k) on a side stream overlaps verify(k-1); "
                                        f"select/verify {args.ctas} CTAs/SM" if args.pipeline_on else
                                        "graph: serial step replayed as one CUDA graph" if args.schedule == "graph"
                                        else "serial")},
@@ -469,11 +479,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-tokens", type=int, default=8192)
     ap.add_argument("--no-spot-check", dest="spot_check", action="store_false")
-    ap.add_argument("--schedule", default="pipeline", choices=["pipeline", "serial", "graph"],
-                    help="pipeline (default): commit(k) on a side stream overlaps verify(k-1) and select(k+1); "
+    ap.add_argument("--schedule", default="partition", choices=["partition", "pipeline", "serial", "graph"],
+                    help="partition (default): the pipeline on two SM partitions (green contexts), commit on "
+                         "--commit-sms SMs, select/verify on the rest; "
+                         "pipeline: commit(k) on a side stream, co-resident with verify(k-1) and select(k+1); "
                          "serial: tl_select, tl_commit, tl_verify back to back; graph: the serial step "
                          "captured as one CUDA graph (api.StepGraph) and replayed")
+    ap.add_argument("--commit-sms", type=int, default=24, help="SMs of the commitment partition (--schedule partition)")
     ap.add_argument("--pipeline", dest="schedule", action="store_const", const="pipeline")
+    ap.add_argument("--partition", dest="schedule", action="store_const", const="partition")
     ap.add_argument("--serial", dest="schedule", action="store_const", const="serial")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak (default): every rank runs the configuration; strong: the configuration's "
@@ -481,7 +495,7 @@ def main():
     ap.add_argument("--ctas", type=int, default=16,
                     help="select/verify one-warp CTAs per SM in pipeline mode (leaves room for the commit CTA)")
     args = ap.parse_args()
-    args.pipeline_on = args.schedule == "pipeline"
+    args.pipeline_on = args.schedule in ("pipeline", "partition")
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
 

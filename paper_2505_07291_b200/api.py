@@ -382,6 +382,8 @@ class Pipeline:
         self.plans = [Plan(eng, row_offsets, H), Plan(eng, row_offsets, H)]
         self.eng = eng
         self.ctas = ctas_per_sm
+        self.co_resident = True
+        self.main = None  # None: the caller's current stream
         self.side = torch.cuda.Stream(eng.device)
 
     def run(self, provers, validators, thresholds: Thresholds = Thresholds(), on_verify=None,
@@ -389,7 +391,11 @@ class Pipeline:
         """provers / validators: sequences of (rows, H) device tensors.  Returns the
         rollout-accept vectors (device uint8) per batch.  ``on_select(k)`` /
         ``on_verify(k)`` are called around the launches (for event timing)."""
-        main = torch.cuda.current_stream(self.eng.device)
+        caller = torch.cuda.current_stream(self.eng.device)
+        main = self.main if self.main is not None else caller
+        if main is not caller:
+            main.wait_stream(caller)
+        self.side.wait_stream(caller)
         n = len(provers)
         out = []
         sel_done = [None] * n
@@ -405,7 +411,7 @@ class Pipeline:
                 sel_done[k] = torch.cuda.Event()
                 sel_done[k].record(main)
                 self.side.wait_event(sel_done[k])
-                pl.commit(self.side, co_resident=True)
+                pl.commit(self.side, co_resident=self.co_resident)
                 com_done[k] = torch.cuda.Event()
                 com_done[k].record(self.side)
             if k >= 1:
@@ -413,10 +419,48 @@ class Pipeline:
                 main.wait_event(com_done[k - 1])
                 if on_verify:
                     on_verify(k - 1, "start", main)
-                out.append(pl.verify(validators[k - 1], None, thresholds, main, self.ctas).clone())
+                acc = pl.verify(validators[k - 1], None, thresholds, main, self.ctas)
+                with torch.cuda.stream(main):
+                    out.append(acc.clone())
                 if on_verify:
                     on_verify(k - 1, "end", main)
+        if main is not caller:
+            caller.wait_stream(main)
+        caller.wait_stream(self.side)
         return out
+
+
+class PartitionedPipeline(Pipeline):
+    """``Pipeline`` on two disjoint SM partitions of the GPU (driver green contexts,
+    ``tl_partition_create``): select / verify at full occupancy on most SMs, the
+    32-warp commitment (128 KiB shared-memory inverse table) on ``commit_sms`` SMs.
+    HBM reads saturate on ~124 of the 148 SMs (tools/lab/greenctx.cu), so the
+    streaming kernels lose little, and the commitment never competes with them for
+    an SM's registers or issue slots.  Results are identical to the serial calls."""
+
+    def __init__(self, eng: "ToplocEngine", row_offsets, H: int, commit_sms: int = 24):
+        super().__init__(eng, row_offsets, H, ctas_per_sm=0)
+        sm, sc = ctypes.c_void_p(), ctypes.c_void_p()
+        nm, nc = ctypes.c_int32(), ctypes.c_int32()
+        with torch.cuda.device(eng.device):
+            _ffi.check(eng.lib.tl_partition_create(int(commit_sms), ctypes.byref(sm), ctypes.byref(sc),
+                                                   ctypes.byref(nm), ctypes.byref(nc)), "tl_partition_create")
+        self._handles = (sm.value, sc.value)
+        self.main = torch.cuda.ExternalStream(sm.value, device=eng.device)
+        self.side = torch.cuda.ExternalStream(sc.value, device=eng.device)
+        self.co_resident = False
+        self.sms = (nm.value, nc.value)  # (streaming, commitment)
+
+    def close(self) -> None:
+        if getattr(self, "_handles", None):
+            _ffi.check(self.eng.lib.tl_partition_destroy(*self._handles), "tl_partition_destroy")
+            self._handles = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 _ENGINES: dict[tuple, ToplocEngine] = {}

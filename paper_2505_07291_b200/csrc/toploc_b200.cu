@@ -15,6 +15,7 @@
 // HBM-bound.  Only the ~0.1 % of elements that can still enter the top-K take the
 // slow path into a shared-memory candidate buffer.
 
+#include <cuda.h>  // driver-API types only; the functions come from cudaGetDriverEntryPoint
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -1183,7 +1184,71 @@ int sm_count() {
   return n;
 }
 
-int sel_grid(int64_t n_chunks, const void* kernel, int ctas_per_sm = 0) {
+// ---- SM partitions (driver green contexts), for the pipelined schedule: the streaming
+// kernels on most SMs, the commitment on a few.  Driver functions are fetched through
+// the runtime (cudaGetDriverEntryPoint), so the library needs no libcuda at link time.
+struct DriverFns {
+  CUresult (*stream_green_ctx)(CUstream, CUgreenCtx*) = nullptr;
+  CUresult (*green_resource)(CUgreenCtx, CUdevResource*, CUdevResourceType) = nullptr;
+  CUresult (*device_get)(CUdevice*, int) = nullptr;
+  CUresult (*device_resource)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
+  CUresult (*split_by_count)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*, unsigned int,
+                             unsigned int) = nullptr;
+  CUresult (*generate_desc)(CUdevResourceDesc*, CUdevResource*, unsigned int) = nullptr;
+  CUresult (*green_create)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int) = nullptr;
+  CUresult (*green_destroy)(CUgreenCtx) = nullptr;
+  CUresult (*green_stream_create)(CUstream*, CUgreenCtx, unsigned int, int) = nullptr;
+  CUresult (*stream_destroy)(CUstream) = nullptr;
+  bool ok = false;
+};
+
+template <typename F>
+bool driver_fn(const char* name, F& f) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+      !p) {
+    cudaGetLastError();
+    return false;
+  }
+  f = reinterpret_cast<F>(p);
+  return true;
+}
+
+const DriverFns& driver() {
+  static const DriverFns fns = [] {
+    DriverFns f;
+    f.ok = driver_fn("cuStreamGetGreenCtx", f.stream_green_ctx) &&
+           driver_fn("cuGreenCtxGetDevResource", f.green_resource) && driver_fn("cuDeviceGet", f.device_get) &&
+           driver_fn("cuDeviceGetDevResource", f.device_resource) &&
+           driver_fn("cuDevSmResourceSplitByCount", f.split_by_count) &&
+           driver_fn("cuDevResourceGenerateDesc", f.generate_desc) && driver_fn("cuGreenCtxCreate", f.green_create) &&
+           driver_fn("cuGreenCtxDestroy", f.green_destroy) &&
+           driver_fn("cuGreenCtxStreamCreate", f.green_stream_create) &&
+           driver_fn("cuStreamDestroy", f.stream_destroy);
+    return f;
+  }();
+  return fns;
+}
+
+// The green context behind a stream, or nullptr for an ordinary stream.
+CUgreenCtx stream_green_ctx(cudaStream_t st) {
+  const DriverFns& d = driver();
+  CUgreenCtx g = nullptr;
+  if (!st || !d.ok || d.stream_green_ctx(reinterpret_cast<CUstream>(st), &g) != CUDA_SUCCESS) return nullptr;
+  return g;
+}
+
+// SMs the kernels launched on `st` can use: its green partition, else the device.
+int stream_sms(cudaStream_t st) {
+  const CUgreenCtx g = stream_green_ctx(st);
+  CUdevResource r;
+  if (g && driver().green_resource(g, &r, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS && r.sm.smCount > 0)
+    return (int)r.sm.smCount;
+  return sm_count();
+}
+
+int sel_grid(int64_t n_chunks, const void* kernel, cudaStream_t st, int ctas_per_sm = 0) {
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSelBlockThreads, kSelSmem) != cudaSuccess ||
       per_sm < 1)
@@ -1191,7 +1256,7 @@ int sel_grid(int64_t n_chunks, const void* kernel, int ctas_per_sm = 0) {
   if (ctas_per_sm > 0 && ctas_per_sm < per_sm) per_sm = ctas_per_sm;
   // one warp per chunk: the fewest warps that finish in the same number of rounds
   // as the full grid (fewer warps share HBM bandwidth, so each round is shorter)
-  const int64_t wmax = (int64_t)sm_count() * per_sm * kSelWarps;
+  const int64_t wmax = (int64_t)stream_sms(st) * per_sm * kSelWarps;
   const int64_t rounds = (n_chunks + wmax - 1) / wmax;
   const int64_t warps = rounds > 0 ? (n_chunks + rounds - 1) / rounds : 1;
   return (int)((warps + kSelWarps - 1) / kSelWarps);
@@ -1206,7 +1271,7 @@ int launch_commit_t(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, 
   if (cudaFuncSetAttribute(commit_kernel<WARPS, HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return TL_ECUDA;
-  int grid = sm_count();
+  int grid = stream_sms(st);  // one CTA per SM of the stream's partition
   if ((int64_t)grid * WARPS > n_chunks) grid = (int)((n_chunks + WARPS - 1) / WARPS);
   commit_kernel<WARPS, HALF><<<grid, WARPS * 32, smem, st>>>(idx, bits, n_chunks, K, tables, proofs, next);
   return launch_status();
@@ -1280,7 +1345,7 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   if (cudaFuncSetAttribute(prove_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
       cudaSuccess)
     return TL_ECUDA;
-  prove_select_kernel<<<sel_grid(n_chunks, (const void*)prove_select_kernel, ctas_per_sm), kSelBlockThreads,
+  prove_select_kernel<<<sel_grid(n_chunks, (const void*)prove_select_kernel, st, ctas_per_sm), kSelBlockThreads,
                         kSelSmem, st>>>(
       a, idx_out, bits_out);
   return launch_status();
@@ -1373,7 +1438,7 @@ int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
     if (cudaFuncSetAttribute(verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
         cudaSuccess)
       return TL_ECUDA;
-    verify_kernel<<<sel_grid(n_chunks, (const void*)verify_kernel, ctas_per_sm), kSelBlockThreads, kSelSmem,
+    verify_kernel<<<sel_grid(n_chunks, (const void*)verify_kernel, st, ctas_per_sm), kSelBlockThreads, kSelSmem,
                     st>>>(
         a, proofs, *thresholds_host, stats_out, accept);
   }
@@ -1394,6 +1459,62 @@ int tl_record_checks(const double* probs, const int64_t* row_off, int32_t n_roll
       verdict_out, frac_out, p_last_out);
   return launch_status();
 }
+
+int tl_partition_create(int32_t commit_sms, void** stream_main_out, void** stream_commit_out, int32_t* main_sms_out,
+                        int32_t* commit_sms_out) {
+  if (commit_sms < 1 || !stream_main_out || !stream_commit_out) return TL_EINVAL;
+  const DriverFns& d = driver();
+  if (!d.ok) return TL_EUNSUPPORTED;
+  int dev_ord = 0;
+  if (cudaGetDevice(&dev_ord) != cudaSuccess || cudaFree(nullptr) != cudaSuccess) return TL_ECUDA;  // primary ctx up
+  CUdevice dev;
+  CUdevResource all, part, rest;
+  unsigned int groups = 1;
+  CUdevResourceDesc d_part, d_rest;
+  CUgreenCtx g_part = nullptr, g_rest = nullptr;
+  CUstream s_part = nullptr, s_rest = nullptr;
+  if (d.device_get(&dev, dev_ord) != CUDA_SUCCESS || d.device_resource(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
+    return TL_EUNSUPPORTED;
+  if ((unsigned)commit_sms >= all.sm.smCount) return TL_EINVAL;
+  if (d.split_by_count(&part, &groups, &all, &rest, 0, (unsigned)commit_sms) != CUDA_SUCCESS || groups != 1 ||
+      rest.sm.smCount == 0)
+    return TL_EUNSUPPORTED;
+  if (d.generate_desc(&d_part, &part, 1) != CUDA_SUCCESS || d.generate_desc(&d_rest, &rest, 1) != CUDA_SUCCESS)
+    return TL_ECUDA;
+  if (d.green_create(&g_part, d_part, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return TL_ECUDA;
+  if (d.green_create(&g_rest, d_rest, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) {
+    d.green_destroy(g_part);
+    return TL_ECUDA;
+  }
+  if (d.green_stream_create(&s_part, g_part, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
+      d.green_stream_create(&s_rest, g_rest, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) {
+    if (s_part) d.stream_destroy(s_part);
+    d.green_destroy(g_part);
+    d.green_destroy(g_rest);
+    return TL_ECUDA;
+  }
+  *stream_main_out = s_rest;
+  *stream_commit_out = s_part;
+  if (main_sms_out) *main_sms_out = (int32_t)rest.sm.smCount;
+  if (commit_sms_out) *commit_sms_out = (int32_t)part.sm.smCount;
+  return TL_OK;
+}
+
+int tl_partition_destroy(void* stream_main, void* stream_commit) {
+  const DriverFns& d = driver();
+  if (!d.ok) return TL_EUNSUPPORTED;
+  for (void* sv : {stream_main, stream_commit}) {
+    if (!sv) continue;
+    cudaStream_t st = static_cast<cudaStream_t>(sv);
+    const CUgreenCtx g = stream_green_ctx(st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return TL_ECUDA;
+    if (d.stream_destroy(reinterpret_cast<CUstream>(st)) != CUDA_SUCCESS) return TL_ECUDA;
+    if (g && d.green_destroy(g) != CUDA_SUCCESS) return TL_ECUDA;
+  }
+  return TL_OK;
+}
+
+int32_t tl_stream_sms(void* stream) { return stream_sms(static_cast<cudaStream_t>(stream)); }
 
 int tl_round6(const void* in, int32_t dtype, int64_t n, double* out, void* stream) {
   if (n < 0 || dtype < 0 || dtype > 3) return TL_EINVAL;

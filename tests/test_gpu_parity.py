@@ -294,9 +294,11 @@ def test_toploc_on_reference_forge_corpus():
                 assert over == [True]
 
 
-def test_pipeline_matches_serial():
-    """The two-stream pipelined schedule (commit(k) overlapping verify(k-1), 3 CTAs/SM,
-    co-resident half-table commitment) gives exactly the serial results."""
+@pytest.mark.parametrize("kind", ["pipeline", "partition"])
+def test_pipeline_matches_serial(kind):
+    """The two-stream pipelined schedules -- commit(k) overlapping verify(k-1), either
+    co-resident (16 one-warp CTAs + the half-table commitment per SM) or on separate SM
+    partitions (green contexts) -- give exactly the serial results."""
     H, offs = 2048, [0, 160, 256, 320]
     n = 5
     prv = [synth_bits(400 * k, 320, H, seed=k, dist=k % 2) for k in range(n)]
@@ -306,9 +308,12 @@ def test_pipeline_matches_serial():
     dp = [torch.from_numpy(b.view(np.int16)).cuda() for b in prv]
     dv = [torch.from_numpy(b.view(np.int16)).cuda() for b in val]
     eng = api.engine()
-    pipe = api.Pipeline(eng, offs, H)
+    pipe = api.Pipeline(eng, offs, H) if kind == "pipeline" else api.PartitionedPipeline(eng, offs, H, commit_sms=16)
     outs = pipe.run(dp, dv)
     torch.cuda.synchronize()
+    if kind == "partition":
+        assert pipe.sms[1] >= 16 and pipe.sms[0] + pipe.sms[1] <= torch.cuda.get_device_properties(0).multi_processor_count
+        assert eng.lib.tl_stream_sms(pipe.main.cuda_stream) == pipe.sms[0]
     for k in range(n):
         pb = eng.prove(dp[k], offs)
         vb = eng.verify(dv[k], offs, pb)
