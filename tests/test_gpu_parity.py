@@ -426,3 +426,35 @@ def test_fuzz_prove_verify_small_shapes(case):
     jit = synth_bits(0, offs[-1], H, seed=case, dist=dist, jitter_thr=int(rng.integers(0, 20000)),
                      jitter_seed=case + 7)
     check_verify_against_oracle(jit, offs, pf, K=K, C=C)
+
+
+def test_many_ragged_rollouts_sampled_against_oracle():
+    """8,000 ragged rollouts (1..100 tokens) at an unaligned H: ~16k
+    chunks through the chunk prefix, the device-side rollout lookup and dynamic chunk
+    claiming.  Every chunk's proof and stats come from the GPU; 300 sampled chunks are
+    re-derived by the oracle."""
+    rng = np.random.default_rng(5)
+    H, R = 333, 8000
+    lens = rng.integers(1, 101, size=R)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    bits = synth_bits(0, int(offs[-1]), H, seed=9, dist=1)
+    jit = synth_bits(0, int(offs[-1]), H, seed=9, dist=1, jitter_thr=3277, jitter_seed=4)
+    eng = api.engine()
+    pb = eng.prove(torch.from_numpy(bits.view(np.int16)).cuda(), offs)
+    vb = eng.verify(torch.from_numpy(jit.view(np.int16)).cuda(), offs, pb)
+    torch.cuda.synchronize()
+    tab = TO.chunk_table(offs, 32)
+    assert pb.proofs.shape[0] == len(tab)
+    proofs = pb.proofs.cpu().numpy()
+    st = vb.stats_host()
+    for j in sorted(rng.choice(len(tab), size=300, replace=False).tolist()):
+        _, s, n = tab[j]
+        _, _, want = TO.prove_chunks([bits[s:s + n].reshape(-1)], 128)
+        assert proofs[j].tobytes() == want[0], f"chunk {j}"
+        o = TO.verify_chunk(jit[s:s + n].reshape(-1), want[0])
+        assert stats_tuple(st[j]) == (o.exp_mismatch, o.n_match, o.mant_sum, o.mant_median, o.accept), f"chunk {j}"
+    # rollout verdict = AND of its chunks
+    acc = vb.chunk_accept.cpu().numpy()
+    co = pb.chunk_offsets
+    want_r = [bool(acc[co[r]:co[r + 1]].all()) for r in range(R)]
+    assert [bool(v) for v in vb.rollout_accept.cpu().tolist()] == want_r
