@@ -49,6 +49,20 @@ for r in rows[2:]:
         if key in hdr:
             i = hdr.index(key)
             out.append(f"| {label} (`{key}`) | {r[i]} | {units[i]} |")
+
+    def val(key):
+        i = hdr.index(key)
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "ms": 1e-3, "us": 1e-6, "ns": 1e-9,
+                 "msecond": 1e-3, "usecond": 1e-6, "nsecond": 1e-9}.get(units[i], 1.0)
+        return float(r[i].replace(",", "")) * scale
+
+    try:
+        gbs = (val("dram__bytes_read.sum") + val("dram__bytes_write.sum")) / val("gpu__time_duration.sum") / 1e9
+        out.append(f"| achieved DRAM bandwidth (read + write) / duration | {gbs:.0f} | GB/s |")
+        out.append(f"| ... of the measured 6,445 GB/s copy peak / the nominal 8,000 GB/s | "
+                   f"{gbs / 6445.3:.3f} / {gbs / 8000:.3f} | |")
+    except (ValueError, ZeroDivisionError):
+        pass
     st = {}
     for i, n in enumerate(hdr):
         if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued"):
@@ -89,6 +103,11 @@ for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
     m = sum(v) / len(v)
     share = f"{m / step * 100:.1f}%" if k.split("<")[0] in STEP and step else ""
     out.append(f"| {k} | {len(v)} | {m:.4f} | {share} |")
+if any(k.startswith("commit_kernel") for k in per):
+    out.append("")
+    out.append("Under ncu the commitment kernel runs on the whole GPU (the profiler's replay does not keep the "
+               "bench's green-context partition), so its time is the standalone one; in the partitioned schedule "
+               "it runs on 24 SMs beside the streaming kernels.")
 if bench:
     out.append("")
     ph = bench.get("phases_ms", {})
