@@ -383,6 +383,7 @@ class Pipeline:
         self.eng = eng
         self.ctas = ctas_per_sm
         self.co_resident = True
+        self.edge_on_main = False  # commit the first and last batch on the main stream
         self.main = None  # None: the caller's current stream
         self.side = torch.cuda.Stream(eng.device)
 
@@ -410,10 +411,16 @@ class Pipeline:
                     on_select(k, "end", main)
                 sel_done[k] = torch.cuda.Event()
                 sel_done[k].record(main)
-                self.side.wait_event(sel_done[k])
-                pl.commit(self.side, co_resident=self.co_resident)
-                com_done[k] = torch.cuda.Event()
-                com_done[k].record(self.side)
+                edge = self.edge_on_main and (k == 0 or k == n - 1)
+                if not edge:
+                    self.side.wait_event(sel_done[k])
+                    pl.commit(self.side, co_resident=self.co_resident)
+                    com_done[k] = torch.cuda.Event()
+                    com_done[k].record(self.side)
+                elif k == 0:  # pipeline fill: nothing to overlap yet, commit on the main SMs
+                    pl.commit(main, co_resident=False)
+                    com_done[k] = torch.cuda.Event()
+                    com_done[k].record(main)
             if k >= 1:
                 pl = self.plans[(k - 1) % 2]
                 main.wait_event(com_done[k - 1])
@@ -424,6 +431,10 @@ class Pipeline:
                     out.append(acc.clone())
                 if on_verify:
                     on_verify(k - 1, "end", main)
+                if self.edge_on_main and k == n - 1:  # pipeline drain: the last commit on the main SMs
+                    self.plans[k % 2].commit(main, co_resident=False)
+                    com_done[k] = torch.cuda.Event()
+                    com_done[k].record(main)
         if main is not caller:
             caller.wait_stream(main)
         caller.wait_stream(self.side)
@@ -449,6 +460,7 @@ class PartitionedPipeline(Pipeline):
         self.main = torch.cuda.ExternalStream(sm.value, device=eng.device)
         self.side = torch.cuda.ExternalStream(sc.value, device=eng.device)
         self.co_resident = False
+        self.edge_on_main = True  # fill and drain: the 124 streaming SMs commit 5x faster than 24
         self.sms = (nm.value, nc.value)  # (streaming, commitment)
 
     def close(self) -> None:
