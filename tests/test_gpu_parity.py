@@ -458,3 +458,14 @@ def test_many_ragged_rollouts_sampled_against_oracle():
     co = pb.chunk_offsets
     want_r = [bool(acc[co[r]:co[r + 1]].all()) for r in range(R)]
     assert [bool(v) for v in vb.rollout_accept.cpu().tolist()] == want_r
+
+
+def test_wide_chunks_rank_with_64_bit_keys():
+    """Chunks of 32 x 20000 = 640,000 elements: indices past 2^19 - 1 cannot use the
+    32-bit chunk-end ranking, so the kernels take the 64-bit path (plus a partial chunk)."""
+    H, offs = 20000, [0, 32, 77]
+    bits = synth_bits(0, offs[-1], H, seed=3, dist=1)
+    check_prove_against_oracle(bits, offs)
+    pf = [bytes(b) for b in gpu_prove(bits, offs).proofs.cpu().numpy()]
+    jit = synth_bits(0, offs[-1], H, seed=3, dist=1, jitter_thr=3277, jitter_seed=8)
+    check_verify_against_oracle(jit, offs, pf)
