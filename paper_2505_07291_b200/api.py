@@ -185,14 +185,26 @@ class ToplocEngine:
             raise ValueError(f"topk must be in [1, {_ffi.TL_MAX_K}]")
         self.lib = _ffi.load()
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self._ws_done: torch.cuda.Event | None = None  # the last call's use of _ws
         self.proof_bytes = 2 + 2 * self.topk
 
     # ----------------------------------------------------------------- plumbing
     def _workspace(self, n_roll: int, n_chunks: int) -> torch.Tensor:
+        """The engine's scratch.  Calls on different streams are ordered on it: the
+        workspace holds the chunk counter and prefix of the running launch, so two calls
+        must never share it concurrently (include/toploc_b200.h)."""
+        cur = torch.cuda.current_stream(self.device)
+        if self._ws_done is not None:
+            cur.wait_event(self._ws_done)
         need = int(self.lib.tl_workspace_bytes(n_roll, n_chunks, self.topk))
         if self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         return self._ws
+
+    def _workspace_used(self) -> None:
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self._ws_done = ev
 
     def _offsets(self, offs: np.ndarray):
         co = np.zeros(len(offs), dtype=np.int64)
@@ -225,6 +237,7 @@ class ToplocEngine:
                                self.topk, n_chunks, proofs.data_ptr(), _ptr(idx), _ptr(vals),
                                ws.data_ptr(), ws.numel(), _stream_handle(self.device))
         _ffi.check(rc, "tl_prove")
+        self._workspace_used()
         return ProofBatch(proofs, offs, co, idx, vals)
 
     # ----------------------------------------------------------------- verify
@@ -245,6 +258,7 @@ class ToplocEngine:
                                 cacc.data_ptr(), racc.data_ptr(), ws.data_ptr(), ws.numel(),
                                 _stream_handle(self.device))
         _ffi.check(rc, "tl_verify")
+        self._workspace_used()
         return VerifyBatch(stats, cacc, racc, co)
 
     def _proof_tensor(self, proofs, n_chunks: int) -> torch.Tensor:

@@ -469,3 +469,22 @@ def test_wide_chunks_rank_with_64_bit_keys():
     pf = [bytes(b) for b in gpu_prove(bits, offs).proofs.cpu().numpy()]
     jit = synth_bits(0, offs[-1], H, seed=3, dist=1, jitter_thr=3277, jitter_seed=8)
     check_verify_against_oracle(jit, offs, pf)
+
+
+def test_engine_calls_on_two_streams_do_not_share_the_workspace_concurrently():
+    """The engine's workspace carries the running launch's chunk counter and prefix;
+    calls issued on different streams are ordered on it, so both stay exact."""
+    H, offs = 2048, [0, 300, 640]
+    a = synth_bits(0, 640, H, seed=21, dist=0)
+    b = synth_bits(0, 640, H, seed=22, dist=1)
+    ta, tb = (torch.from_numpy(x.view(np.int16)).cuda() for x in (a, b))
+    eng = api.engine()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            pa = eng.prove(ta, offs)
+        with torch.cuda.stream(s2):
+            pb = eng.prove(tb, offs)
+        torch.cuda.synchronize()
+        assert pa.to_bytes() == TO.build_proofs(a, offs)
+        assert pb.to_bytes() == TO.build_proofs(b, offs)
