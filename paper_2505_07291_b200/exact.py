@@ -15,6 +15,7 @@ split, not a fallback: without the CUDA library the call raises.
 from __future__ import annotations
 
 import hashlib
+import threading
 
 import numpy as np
 import torch
@@ -78,6 +79,7 @@ def build_commitments(hidden, k: int = 32) -> list[bytes]:
 
 
 _STAGING: dict = {}
+_STAGING_LOCK = threading.Lock()  # one build_commitments_batch at a time uses the staging
 
 
 def release_staging() -> None:
@@ -109,9 +111,6 @@ def build_commitments_batch(hidden, row_offsets, k: int = 32, threads: int | Non
     serial-per-rollout SHA-256 chains of different rollouts run on all host cores
     while the next group is rounded and copied.  Byte-identical to
     ``build_commitments`` per rollout (rollout.py:51-68)."""
-    import concurrent.futures as cf
-    import os
-
     if k < 1:
         raise ValueError("interval must be >= 1")
     if not torch.cuda.is_available():
@@ -126,8 +125,6 @@ def build_commitments_batch(hidden, row_offsets, k: int = 32, threads: int | Non
     if offs[0] != 0 or offs[-1] != n_rows or np.any(np.diff(offs) < 0):
         raise ValueError("row_offsets must start at 0, be non-decreasing and end at n_rows")
     dev = torch.device("cuda", torch.cuda.current_device())
-    lib = _ffi.load()
-    side = torch.cuda.Stream(dev)
     R = len(offs) - 1
     # groups of whole rollouts, ~group_rows rows each
     groups, start = [], 0
@@ -138,6 +135,16 @@ def build_commitments_batch(hidden, row_offsets, k: int = 32, threads: int | Non
         groups.append((start, end))
         start = end
     max_rows = max((int(offs[e] - offs[b]) for b, e in groups), default=0)
+    with _STAGING_LOCK:
+        return _batch_locked(t, offs, k, threads, groups, max_rows, H, R, dev)
+
+
+def _batch_locked(t, offs, k, threads, groups, max_rows, H, R, dev):
+    import concurrent.futures as cf
+    import os
+
+    lib = _ffi.load()
+    side = torch.cuda.Stream(dev)
     dbuf, hbuf = _staging(dev, max(max_rows, 1) * H)
     dbuf = [d[:max(max_rows, 1) * H].view(max(max_rows, 1), H) for d in dbuf]
     hbuf = [h[:max(max_rows, 1) * H].view(max(max_rows, 1), H) for h in hbuf]
