@@ -285,7 +285,8 @@ def run_b200(args, cfg, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    sel_ev, ver_ev = {}, {}
+    sel_ev, ver_ev, com_ev = {}, {}, {}
+    side_ms = None
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
@@ -299,12 +300,17 @@ def run_b200(args, cfg, rank, world, local_rank):
                 store.setdefault(k, {})[what] = ev
             return f
         t_start.record(stream)
-        outs = pipe.run([prv] * args.steps, [val] * args.steps, on_select=mark(sel_ev), on_verify=mark(ver_ev))
+        outs = pipe.run([prv] * args.steps, [val] * args.steps, on_select=mark(sel_ev), on_verify=mark(ver_ev),
+                        on_commit=mark(com_ev))
         t_end.record(stream)
         torch.cuda.synchronize(dev)
         sel_ms = sum(v["start"].elapsed_time(v["end"]) for v in sel_ev.values()) / args.steps
         ver_ms = sum(v["start"].elapsed_time(v["end"]) for v in ver_ev.values()) / args.steps
         com_ms = serial_ms["commit"]
+        # the commitments as they ran beside the streams (side stream / partition; the first
+        # and last of a partitioned run ran on the streaming SMs)
+        side = [v["start"].elapsed_time(v["end"]) for k, v in sorted(com_ev.items())[1:-1]]
+        side_ms = sum(side) / len(side) if side else None
         accepted = int(outs[-1].sum().item())
         assert all(int(o.sum().item()) == accepted for o in outs)
         spot_pipe = bool(torch.equal(pipe.plans[(args.steps - 1) % 2].proofs, plan.proofs))
@@ -447,6 +453,7 @@ def run_b200(args, cfg, rank, world, local_rank):
                               # report both denominators; the primary is the measured peak
                               "frac_of_nominal_8tbs": value / world * algorithmic_bytes_per_token(H) / 1e9 / NOMINAL_GBS},
             "phases_ms": {"select": sel_ms, "commit": com_ms, "verify": ver_ms,
+                          "commit_beside_streams": side_ms if pipe is not None else None,
                           "verify_gbs": ver_bytes / (ver_ms / 1e3) / 1e9, "verdict_gather": gather_ms,
                           "serial": serial_ms,
                           "schedule": (f"partitioned: commit on {pipe.sms[1]} SMs, select/verify on {pipe.sms[0]} SMs "

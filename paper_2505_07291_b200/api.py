@@ -402,10 +402,10 @@ class Pipeline:
         self.side = torch.cuda.Stream(eng.device)
 
     def run(self, provers, validators, thresholds: Thresholds = Thresholds(), on_verify=None,
-            on_select=None) -> list[torch.Tensor]:
+            on_select=None, on_commit=None) -> list[torch.Tensor]:
         """provers / validators: sequences of (rows, H) device tensors.  Returns the
-        rollout-accept vectors (device uint8) per batch.  ``on_select(k)`` /
-        ``on_verify(k)`` are called around the launches (for event timing)."""
+        rollout-accept vectors (device uint8) per batch.  ``on_select(k, what, stream)`` /
+        ``on_commit`` / ``on_verify`` are called around the launches (for event timing)."""
         caller = torch.cuda.current_stream(self.eng.device)
         main = self.main if self.main is not None else caller
         if main is not caller:
@@ -428,13 +428,9 @@ class Pipeline:
                 edge = self.edge_on_main and (k == 0 or k == n - 1)
                 if not edge:
                     self.side.wait_event(sel_done[k])
-                    pl.commit(self.side, co_resident=self.co_resident)
-                    com_done[k] = torch.cuda.Event()
-                    com_done[k].record(self.side)
+                    self._commit(pl, k, self.side, self.co_resident, on_commit, com_done)
                 elif k == 0:  # pipeline fill: nothing to overlap yet, commit on the main SMs
-                    pl.commit(main, co_resident=False)
-                    com_done[k] = torch.cuda.Event()
-                    com_done[k].record(main)
+                    self._commit(pl, k, main, False, on_commit, com_done)
             if k >= 1:
                 pl = self.plans[(k - 1) % 2]
                 main.wait_event(com_done[k - 1])
@@ -446,13 +442,21 @@ class Pipeline:
                 if on_verify:
                     on_verify(k - 1, "end", main)
                 if self.edge_on_main and k == n - 1:  # pipeline drain: the last commit on the main SMs
-                    self.plans[k % 2].commit(main, co_resident=False)
-                    com_done[k] = torch.cuda.Event()
-                    com_done[k].record(main)
+                    self._commit(self.plans[k % 2], k, main, False, on_commit, com_done)
         if main is not caller:
             caller.wait_stream(main)
         caller.wait_stream(self.side)
         return out
+
+    @staticmethod
+    def _commit(pl: "Plan", k: int, stream, co_resident: bool, on_commit, com_done) -> None:
+        if on_commit:
+            on_commit(k, "start", stream)
+        pl.commit(stream, co_resident=co_resident)
+        if on_commit:
+            on_commit(k, "end", stream)
+        com_done[k] = torch.cuda.Event()
+        com_done[k].record(stream)
 
 
 class PartitionedPipeline(Pipeline):
