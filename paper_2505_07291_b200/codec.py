@@ -21,7 +21,6 @@ import numpy as np
 TOPLOC_INTERVAL = 32
 PROOF_BYTES = 258
 PROOF_HEX = 2 * PROOF_BYTES
-_HEX = np.frombuffer(b"0123456789abcdef", dtype=np.uint8)
 
 
 class ProofFormatError(ValueError):
@@ -68,11 +67,8 @@ def encode(proofs, row_offsets=None, chunk_offsets=None) -> list[list[str]]:
     co = np.asarray(chunk_offsets, dtype=np.int64)
     if co[0] != 0 or co[-1] != arr.shape[0] or np.any(np.diff(co) < 0):
         raise ProofFormatError("chunk offsets do not tile the proofs")
-    # vectorised hex: two nibbles per byte through a 16-entry table
-    hexed = np.empty((arr.shape[0], PROOF_HEX), dtype=np.uint8)
-    hexed[:, 0::2] = _HEX[arr >> 4]
-    hexed[:, 1::2] = _HEX[arr & 15]
-    rows = [bytes(r).decode("ascii") for r in hexed]
+    text = arr.tobytes().hex()  # one C-level hex pass, then string slices
+    rows = [text[i:i + PROOF_HEX] for i in range(0, len(text), PROOF_HEX)]
     return [rows[int(co[r]):int(co[r + 1])] for r in range(len(co) - 1)]
 
 
@@ -82,7 +78,7 @@ def decode(commitments, n_tokens=None, interval: int = TOPLOC_INTERVAL) -> tuple
     Checks each item is 516 hex characters and, when ``n_tokens`` (one per rollout)
     is given, that every list has ``ceil(T / interval)`` items."""
     check_interval(interval)
-    counts, blobs = [], []
+    counts, texts = [], []
     for r, items in enumerate(commitments):
         items = list(items)
         if n_tokens is not None:
@@ -92,14 +88,24 @@ def decode(commitments, n_tokens=None, interval: int = TOPLOC_INTERVAL) -> tuple
         for i, s in enumerate(items):
             if not isinstance(s, str) or len(s) != PROOF_HEX:
                 raise ProofFormatError(f"rollout {r} item {i}: not a {PROOF_HEX}-char proof")
-            try:
-                blobs.append(bytes.fromhex(s))
-            except ValueError:
-                raise ProofFormatError(f"rollout {r} item {i}: not hex") from None
+        texts.extend(items)
         counts.append(len(items))
-    arr = np.frombuffer(b"".join(blobs), dtype=np.uint8).reshape(-1, PROOF_BYTES).copy() if blobs else \
-        np.zeros((0, PROOF_BYTES), dtype=np.uint8)
+    try:  # one C-level parse of the concatenation
+        blob = bytes.fromhex("".join(texts))
+    except ValueError:
+        bad = next(i for i, s in enumerate(texts) if not _is_hex(s))
+        r = int(np.searchsorted(np.cumsum(counts), bad, side="right"))
+        raise ProofFormatError(f"rollout {r} item {bad - int(np.sum(counts[:r]))}: not hex") from None
+    arr = np.frombuffer(blob, dtype=np.uint8).reshape(-1, PROOF_BYTES).copy()
     return arr, np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+
+
+def _is_hex(s: str) -> bool:
+    try:
+        bytes.fromhex(s)
+        return True
+    except ValueError:
+        return False
 
 
 def modulus(proof_hex_or_bytes) -> int:
