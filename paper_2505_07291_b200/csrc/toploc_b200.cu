@@ -1031,24 +1031,39 @@ __global__ void rollout_verdict_kernel(const uint8_t* __restrict__ chunk_accept,
 }
 
 // ----------------------------------------------------------------------------- record checks
-// One warp per record: termination (checks.py:120-131), sampling (checks.py:134-142),
-// commitment verdict, in the reference's order.  The sampling fraction is the exact
-// count of probs < p_low divided once in float64, like np.mean over a bool array.
-__global__ void record_checks_kernel(const double* __restrict__ probs, const int64_t* __restrict__ row_off,
+// One 256-thread CTA per record (grid-stride over records): termination
+// (checks.py:120-131), sampling (checks.py:134-142), commitment verdict, in the
+// reference's order.  The sampling fraction is the exact count of probs < p_low
+// divided once in float64, like np.mean over a bool array.  Each thread counts a
+// strided share with 4 independent loads in flight; a warp reduction and one shared
+// word per warp finish the count.
+constexpr int kRecThreads = 256;
+__global__ void __launch_bounds__(kRecThreads) record_checks_kernel(const double* __restrict__ probs, const int64_t* __restrict__ row_off,
                                      int n_roll, const int32_t* __restrict__ prompt_len,
                                      const uint8_t* __restrict__ ends_with_eos, tl_record_thresholds th,
                                      const uint8_t* __restrict__ commit_accept,
                                      const uint8_t* __restrict__ commit_checked, int32_t* __restrict__ verdict_out,
                                      double* __restrict__ frac_out, double* __restrict__ p_last_out) {
-  const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (r >= n_roll) return;
+  __shared__ unsigned long long part[kRecThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int r = blockIdx.x; r < n_roll; r += gridDim.x) {
   const int64_t lo = row_off[r], T = row_off[r + 1] - lo;
   unsigned long long cnt = 0;
-  for (int64_t i = lane; i < T; i += 32) cnt += probs[lo + i] < th.p_low ? 1ull : 0ull;
+  int64_t i = tid;
+  for (; i + 3 * kRecThreads < T; i += 4 * kRecThreads) {
+    const double a = probs[lo + i], b = probs[lo + i + kRecThreads];
+    const double c = probs[lo + i + 2 * kRecThreads], d = probs[lo + i + 3 * kRecThreads];
+    cnt += (a < th.p_low) + (b < th.p_low) + (c < th.p_low) + (d < th.p_low);
+  }
+  for (; i < T; i += kRecThreads) cnt += probs[lo + i] < th.p_low ? 1ull : 0ull;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
-  if (lane != 0) return;
+  if (lane == 0) part[tid >> 5] = cnt;
+  __syncthreads();
+  if (tid == 0) {
+  cnt = 0;
+#pragma unroll
+  for (int w = 0; w < kRecThreads / 32; ++w) cnt += part[w];
   const double frac = T > 0 ? __ddiv_rn((double)cnt, (double)T) : 0.0;
   const double p_last = T > 0 ? probs[lo + T - 1] : __longlong_as_double(0x7FF8000000000000ll);
   const bool term_ok = (int64_t)prompt_len[r] + T >= (int64_t)th.max_len ||
@@ -1059,6 +1074,9 @@ __global__ void record_checks_kernel(const double* __restrict__ probs, const int
   verdict_out[r] = !term_ok ? 1 : !samp_ok ? 2 : !com_ok ? 3 : 0;
   if (frac_out) frac_out[r] = frac;
   if (p_last_out) p_last_out[r] = p_last;
+  }
+  __syncthreads();  // part[] is reused by the next record
+  }
 }
 
 // ----------------------------------------------------------------------------- exact mode
@@ -1454,7 +1472,9 @@ int tl_record_checks(const double* probs, const int64_t* row_off, int32_t n_roll
   if (n_roll < 0 || !thresholds_host) return TL_EINVAL;
   if (n_roll == 0) return TL_OK;
   if (!probs || !row_off || !prompt_len || !ends_with_eos || !verdict_out) return TL_EINVAL;
-  record_checks_kernel<<<(n_roll + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  const int max_grid = stream_sms(static_cast<cudaStream_t>(stream)) * 8;
+  const int grid = n_roll < max_grid ? n_roll : max_grid;
+  record_checks_kernel<<<grid, kRecThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       probs, row_off, n_roll, prompt_len, ends_with_eos, *thresholds_host, commit_accept, commit_checked,
       verdict_out, frac_out, p_last_out);
   return launch_status();
