@@ -145,16 +145,16 @@ int tl_verify(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, in
               size_t workspace_bytes, void* stream);
 
 /*
- * SM partition for the pipelined schedule (driver green contexts): two streams on
- * disjoint SM sets of the current device -- commit_sms SMs (rounded up to the
- * driver's granularity, 8 on sm_100) for tl_commit, the rest for tl_select /
- * tl_verify.  Every entry point sizes its grid to the partition of the stream it
- * is given (tl_stream_sms).  Returns TL_EUNSUPPORTED where the driver has no green
- * contexts.  tl_partition_destroy synchronises and frees both.
+ * SM partition for the pipelined schedule (driver green contexts): streams on two
+ * disjoint SM sets of the current device.  streams_out[3]: two streams on the
+ * streaming partition (select, verify) and one on the commit_sms partition (rounded
+ * up to the driver's granularity, 8 on sm_100); sms_out[2] (nullable): SMs of the
+ * streaming and the commitment partition.  Every entry point sizes its grid to the
+ * partition of the stream it is given (tl_stream_sms).  Returns TL_EUNSUPPORTED where
+ * the driver has no green contexts.  tl_partition_destroy synchronises and frees.
  */
-int tl_partition_create(int32_t commit_sms, void** stream_main_out, void** stream_commit_out,
-                        int32_t* main_sms_out, int32_t* commit_sms_out);
-int tl_partition_destroy(void* stream_main, void* stream_commit);
+int tl_partition_create(int32_t commit_sms, void** streams_out, int32_t* sms_out);
+int tl_partition_destroy(void** streams);
 int32_t tl_stream_sms(void* stream);
 
 /*

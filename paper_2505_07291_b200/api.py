@@ -337,15 +337,19 @@ class Plan:
         return self.proofs
 
     def verify(self, h: torch.Tensor, proofs: torch.Tensor | None = None,
-               thresholds: Thresholds = Thresholds(), stream=None, ctas_per_sm: int = 0) -> torch.Tensor:
+               thresholds: Thresholds = Thresholds(), stream=None, ctas_per_sm: int = 0,
+               workspace: torch.Tensor | None = None) -> torch.Tensor:
+        """tl_verify; ``workspace`` (same size as ``ws``) lets a verify run concurrently
+        with this plan's select on another stream."""
         h = self._check_hidden(h)
         e = self.eng
         pr = self.proofs if proofs is None else proofs
+        ws = self.ws if workspace is None else workspace
         th = thresholds.to_c()
         _ffi.check(e.lib.tl_verify_ex(h.data_ptr(), self.offs_dev.data_ptr(), self.n_roll, self.n_rows, self.H,
                                       e.chunk, e.topk, self.n_chunks, pr.data_ptr(), ctypes.byref(th),
                                       self.stats.data_ptr(), self.chunk_accept.data_ptr(),
-                                      self.rollout_accept.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                                      self.rollout_accept.data_ptr(), ws.data_ptr(), ws.numel(),
                                       ctas_per_sm, self._stream(stream)), "tl_verify")
         return self.rollout_accept
 
@@ -460,30 +464,79 @@ class Pipeline:
 
 
 class PartitionedPipeline(Pipeline):
-    """``Pipeline`` on two disjoint SM partitions of the GPU (driver green contexts,
-    ``tl_partition_create``): select / verify at full occupancy on most SMs, the
-    32-warp commitment (128 KiB shared-memory inverse table) on ``commit_sms`` SMs.
-    HBM reads saturate on ~124 of the 148 SMs (tools/lab/greenctx.cu), so the
-    streaming kernels lose little, and the commitment never competes with them for
-    an SM's registers or issue slots.  Results are identical to the serial calls."""
+    """Prove + verify a stream of batches on two disjoint SM partitions of the GPU (driver
+    green contexts, ``tl_partition_create``).
+
+    - The 32-warp commitment (128 KiB shared-memory inverse table) runs on
+      ``commit_sms`` SMs; it never competes with the streams for an SM.
+    - select and verify run at full occupancy on the other SMs, on two streams:
+      select(k) on one, verify(k-2) on the other, with commit(k-1) on the partition.
+      Persistent kernels on one stream leave their tail idle; the other stream's next
+      kernel fills it.  HBM reads saturate on ~124 of the 148 SMs (tools/lab/greenctx.cu).
+    - Three buffer sets rotate; each verify has its own workspace.
+    Results are identical to the serial calls."""
 
     def __init__(self, eng: "ToplocEngine", row_offsets, H: int, commit_sms: int = 24):
         super().__init__(eng, row_offsets, H, ctas_per_sm=0)
-        sm, sc = ctypes.c_void_p(), ctypes.c_void_p()
-        nm, nc = ctypes.c_int32(), ctypes.c_int32()
+        self.plans.append(Plan(eng, row_offsets, H))
+        self.ws_verify = [torch.empty_like(p.ws) for p in self.plans]
+        streams = (ctypes.c_void_p * 3)()
+        sms = (ctypes.c_int32 * 2)()
         with torch.cuda.device(eng.device):
-            _ffi.check(eng.lib.tl_partition_create(int(commit_sms), ctypes.byref(sm), ctypes.byref(sc),
-                                                   ctypes.byref(nm), ctypes.byref(nc)), "tl_partition_create")
-        self._handles = (sm.value, sc.value)
-        self.main = torch.cuda.ExternalStream(sm.value, device=eng.device)
-        self.side = torch.cuda.ExternalStream(sc.value, device=eng.device)
+            _ffi.check(eng.lib.tl_partition_create(int(commit_sms), streams, sms), "tl_partition_create")
+        self._handles = streams
+        self.main = torch.cuda.ExternalStream(streams[0], device=eng.device)   # select
+        self.vstream = torch.cuda.ExternalStream(streams[1], device=eng.device)  # verify
+        self.side = torch.cuda.ExternalStream(streams[2], device=eng.device)   # commit
         self.co_resident = False
-        self.edge_on_main = True  # fill and drain: the 124 streaming SMs commit 5x faster than 24
-        self.sms = (nm.value, nc.value)  # (streaming, commitment)
+        self.sms = (sms[0], sms[1])  # (streaming, commitment)
+
+    def run(self, provers, validators, thresholds: Thresholds = Thresholds(), on_verify=None,
+            on_select=None, on_commit=None) -> list[torch.Tensor]:
+        caller = torch.cuda.current_stream(self.eng.device)
+        sel, ver, side = self.main, self.vstream, self.side
+        for st in (sel, ver, side):
+            st.wait_stream(caller)
+        n = len(provers)
+        out = []
+        com_done = [None] * n
+        ver_done = [None] * n
+        for k in range(n + 2):
+            if k < n:
+                pl = self.plans[k % 3]
+                if k >= 3:
+                    sel.wait_event(com_done[k - 3])  # this plan's idx / bits consumed
+                if on_select:
+                    on_select(k, "start", sel)
+                pl.select(provers[k], sel, self.ctas)
+                if on_select:
+                    on_select(k, "end", sel)
+                done = torch.cuda.Event()
+                done.record(sel)
+                side.wait_event(done)
+                if k >= 3:
+                    side.wait_event(ver_done[k - 3])  # this plan's proofs read
+                self._commit(pl, k, side, False, on_commit, com_done)
+            if k >= 2:
+                j = k - 2
+                pl = self.plans[j % 3]
+                ver.wait_event(com_done[j])
+                if on_verify:
+                    on_verify(j, "start", ver)
+                acc = pl.verify(validators[j], None, thresholds, ver, self.ctas, workspace=self.ws_verify[j % 3])
+                with torch.cuda.stream(ver):
+                    out.append(acc.clone())
+                if on_verify:
+                    on_verify(j, "end", ver)
+                ver_done[j] = torch.cuda.Event()
+                ver_done[j].record(ver)
+        for st in (sel, ver, side):
+            caller.wait_stream(st)
+        return out
 
     def close(self) -> None:
-        if getattr(self, "_handles", None):
-            _ffi.check(self.eng.lib.tl_partition_destroy(*self._handles), "tl_partition_destroy")
+        if getattr(self, "_handles", None) is not None:
+            _ffi.check(self.eng.lib.tl_partition_destroy(self._handles), "tl_partition_destroy")
             self._handles = None
 
     def __del__(self):

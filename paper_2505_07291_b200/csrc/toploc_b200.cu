@@ -1480,9 +1480,8 @@ int tl_record_checks(const double* probs, const int64_t* row_off, int32_t n_roll
   return launch_status();
 }
 
-int tl_partition_create(int32_t commit_sms, void** stream_main_out, void** stream_commit_out, int32_t* main_sms_out,
-                        int32_t* commit_sms_out) {
-  if (commit_sms < 1 || !stream_main_out || !stream_commit_out) return TL_EINVAL;
+int tl_partition_create(int32_t commit_sms, void** streams_out, int32_t* sms_out) {
+  if (commit_sms < 1 || !streams_out) return TL_EINVAL;
   const DriverFns& d = driver();
   if (!d.ok) return TL_EUNSUPPORTED;
   int dev_ord = 0;
@@ -1492,7 +1491,7 @@ int tl_partition_create(int32_t commit_sms, void** stream_main_out, void** strea
   unsigned int groups = 1;
   CUdevResourceDesc d_part, d_rest;
   CUgreenCtx g_part = nullptr, g_rest = nullptr;
-  CUstream s_part = nullptr, s_rest = nullptr;
+  CUstream s[3] = {nullptr, nullptr, nullptr};
   if (d.device_get(&dev, dev_ord) != CUDA_SUCCESS || d.device_resource(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
     return TL_EUNSUPPORTED;
   if ((unsigned)commit_sms >= all.sm.smCount) return TL_EINVAL;
@@ -1506,30 +1505,39 @@ int tl_partition_create(int32_t commit_sms, void** stream_main_out, void** strea
     d.green_destroy(g_part);
     return TL_ECUDA;
   }
-  if (d.green_stream_create(&s_part, g_part, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
-      d.green_stream_create(&s_rest, g_rest, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) {
-    if (s_part) d.stream_destroy(s_part);
+  if (d.green_stream_create(&s[0], g_rest, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
+      d.green_stream_create(&s[1], g_rest, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
+      d.green_stream_create(&s[2], g_part, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) {
+    for (CUstream x : s)
+      if (x) d.stream_destroy(x);
     d.green_destroy(g_part);
     d.green_destroy(g_rest);
     return TL_ECUDA;
   }
-  *stream_main_out = s_rest;
-  *stream_commit_out = s_part;
-  if (main_sms_out) *main_sms_out = (int32_t)rest.sm.smCount;
-  if (commit_sms_out) *commit_sms_out = (int32_t)part.sm.smCount;
+  for (int q = 0; q < 3; ++q) streams_out[q] = s[q];
+  if (sms_out) {
+    sms_out[0] = (int32_t)rest.sm.smCount;
+    sms_out[1] = (int32_t)part.sm.smCount;
+  }
   return TL_OK;
 }
 
-int tl_partition_destroy(void* stream_main, void* stream_commit) {
+int tl_partition_destroy(void** streams) {
   const DriverFns& d = driver();
   if (!d.ok) return TL_EUNSUPPORTED;
-  for (void* sv : {stream_main, stream_commit}) {
-    if (!sv) continue;
-    cudaStream_t st = static_cast<cudaStream_t>(sv);
-    const CUgreenCtx g = stream_green_ctx(st);
+  if (!streams) return TL_EINVAL;
+  CUgreenCtx ctx[3] = {nullptr, nullptr, nullptr};
+  for (int q = 0; q < 3; ++q) {
+    if (!streams[q]) continue;
+    cudaStream_t st = static_cast<cudaStream_t>(streams[q]);
+    ctx[q] = stream_green_ctx(st);
     if (cudaStreamSynchronize(st) != cudaSuccess) return TL_ECUDA;
     if (d.stream_destroy(reinterpret_cast<CUstream>(st)) != CUDA_SUCCESS) return TL_ECUDA;
-    if (g && d.green_destroy(g) != CUDA_SUCCESS) return TL_ECUDA;
+  }
+  for (int q = 0; q < 3; ++q) {  // the two streaming streams share one context
+    bool seen = false;
+    for (int r = 0; r < q; ++r) seen = seen || ctx[r] == ctx[q];
+    if (ctx[q] && !seen && d.green_destroy(ctx[q]) != CUDA_SUCCESS) return TL_ECUDA;
   }
   return TL_OK;
 }

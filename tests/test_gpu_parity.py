@@ -319,7 +319,7 @@ def test_pipeline_matches_serial(kind):
         vb = eng.verify(dv[k], offs, pb)
         assert outs[k].cpu().tolist() == vb.rollout_accept.cpu().tolist(), k
         assert pb.to_bytes() == TO.build_proofs(prv[k], offs)
-    assert torch.equal(pipe.plans[(n - 1) % 2].proofs, eng.prove(dp[n - 1], offs).proofs)
+    assert torch.equal(pipe.plans[(n - 1) % len(pipe.plans)].proofs, eng.prove(dp[n - 1], offs).proofs)
     assert outs[3].cpu().tolist() == [0, 0, 0]
 
 
