@@ -488,3 +488,23 @@ def test_engine_calls_on_two_streams_do_not_share_the_workspace_concurrently():
         torch.cuda.synchronize()
         assert pa.to_bytes() == TO.build_proofs(a, offs)
         assert pb.to_bytes() == TO.build_proofs(b, offs)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_partitioned_pipeline_short_runs(n):
+    """Fill and drain of the dual-stream partitioned schedule (verify two batches behind
+    select, three buffer sets) for runs shorter than, equal to and just past the lag."""
+    H, offs = 1024, [0, 96, 200]
+    prv = [synth_bits(300 * k, 200, H, seed=30 + k, dist=k % 2) for k in range(n)]
+    val = [synth_bits(300 * k, 200, H, seed=30 + k, dist=k % 2, jitter_thr=3277, jitter_seed=k) for k in range(n)]
+    dp = [torch.from_numpy(b.view(np.int16)).cuda() for b in prv]
+    dv = [torch.from_numpy(b.view(np.int16)).cuda() for b in val]
+    eng = api.engine()
+    pipe = api.PartitionedPipeline(eng, offs, H, commit_sms=16)
+    outs = pipe.run(dp, dv)
+    torch.cuda.synchronize()
+    assert len(outs) == n
+    for k in range(n):
+        vb = eng.verify(dv[k], offs, eng.prove(dp[k], offs))
+        assert outs[k].cpu().tolist() == vb.rollout_accept.cpu().tolist(), k
+    pipe.close()
