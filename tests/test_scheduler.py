@@ -10,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2505_07291_b200.scheduler import gather_verdicts, plan, shard_by_tokens
+from paper_2505_07291_b200.scheduler import gather_verdicts, gather_verdicts_lpt, plan, shard_by_tokens, shard_lpt
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
@@ -38,6 +38,21 @@ def test_shards_degenerate():
         shard_by_tokens([1, 2], 0)
 
 
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_lpt_partitions_and_balances_ragged_batches(world):
+    rng = np.random.default_rng(world)
+    lengths = np.concatenate([rng.integers(1, 500, size=60), [40000, 39000, 20000]])  # a few very long
+    shards = shard_lpt(lengths, world)
+    allidx = np.sort(np.concatenate(shards))
+    assert np.array_equal(allidx, np.arange(lengths.size))           # a partition
+    loads = [int(lengths[s].sum()) for s in shards]
+    # LPT bound: makespan <= 4/3 OPT, OPT >= max(mean load, longest job)
+    opt_lb = max(lengths.sum() / world, lengths.max())
+    assert max(loads) <= 4 / 3 * opt_lb + 1
+    contiguous = [int(lengths[lo:hi].sum()) for lo, hi in shard_by_tokens(lengths, world)]
+    assert max(loads) <= max(contiguous)
+
+
 def test_plan_local_offsets():
     offs = np.array([0, 10, 30, 30, 60, 100])
     sp = plan(np.diff(offs), rank=1, world=2)
@@ -49,6 +64,18 @@ def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
+
+
+def _worker_lpt(rank, world, port, lengths, truth, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shards = shard_lpt(lengths, world)
+        local = torch.tensor([truth[i] for i in shards[rank]], dtype=torch.uint8)
+        q.put((rank, gather_verdicts_lpt(local, shards).tolist()))
+    finally:
+        dist.destroy_process_group()
 
 
 def _worker(rank, world, port, lengths, truth, q):
@@ -79,5 +106,22 @@ def test_gloo_gather_matches_single_process(world):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    for _, full in out:
+        assert full == truth
+
+
+def test_gloo_lpt_gather_restores_rollout_order():
+    rng = np.random.default_rng(9)
+    lengths = rng.integers(1, 9000, size=29)
+    truth = (rng.random(29) < 0.6).astype(np.uint8).tolist()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_lpt, args=(r, 2, port, lengths, truth, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
     for _, full in out:
         assert full == truth
