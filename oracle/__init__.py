@@ -13,5 +13,8 @@ Nothing in ``paper_2505_07291_b200`` may import this package.  Only ``tests/``,
   is absent from this machine, so TOPLOC parity is UNPINNED against upstream;
   the oracle is pinned against mathematical properties and independent
   restatements (see its module docstring and DESIGN.md section 3).
+* ``checks_oracle`` -- restatement of the validator's prefill-sharing record checks
+  (``swarm/validator/checks.py:120-142,204-213``).  Parity PINNED against the
+  reference's own ``check_termination`` / ``check_sampling`` (``tests/test_oracle_checks.py``).
 * ``synth_cpu``     -- CPU twin of the on-device synthetic hidden-state generator.
 """
