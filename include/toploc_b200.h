@@ -196,6 +196,18 @@ int tl_record_checks(const double* probs, const int64_t* row_off, int32_t n_roll
 int tl_round6(const void* in, int32_t dtype, int64_t n, double* out, void* stream);
 
 /*
+ * Exact mode, whole chains on the GPU: for each rollout r of `hidden` (dtype as
+ * tl_round6, rows delimited by row_off, device int64 [n_roll+1]), the reference's
+ * commitment chain d_j = SHA-256(d_{j-1} || LE-f64(round(block_j, 6))) over k-row
+ * blocks (one digest for T = 0).  digest_off (device int64 [n_roll]) gives each
+ * rollout's first digest; digests_out receives 32 bytes per digest.  One thread per
+ * rollout: faster than host SHA once a batch has many rollouts.
+ */
+int tl_exact_chains(const void* hidden, int32_t dtype, const int64_t* row_off, int32_t n_roll,
+                    int32_t H, int32_t k, const int64_t* digest_off, uint8_t* digests_out,
+                    void* stream);
+
+/*
  * Synthetic bf16 hidden states (bench/test input; counter-based, CPU-replayable,
  * see paper_2505_07291_b200/synth.py).  normal_table: device uint16[65536].
  * massive: 6 channel ids (dist 1).  jitter_thr/65536 of elements get +-1 in

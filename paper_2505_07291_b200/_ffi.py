@@ -54,6 +54,7 @@ SYMBOLS = {
     "tl_verify": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_i64, c_vp,
                           ctypes.POINTER(Thresholds), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "tl_round6": (c_i32, [c_vp, c_i32, c_i64, c_vp, c_vp]),
+    "tl_exact_chains": (c_i32, [c_vp, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "tl_partition_create": (c_i32, [c_i32, c_vp, c_vp]),
     "tl_partition_destroy": (c_i32, [c_vp]),
     "tl_stream_sms": (c_i32, [c_vp]),

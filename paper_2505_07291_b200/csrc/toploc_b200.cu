@@ -1120,6 +1120,117 @@ __global__ void round6_kernel(const void* __restrict__ in, int dtype, int64_t n,
   }
 }
 
+// ----------------------------------------------------------------------------- exact mode on the GPU
+// The reference's commitment chain (rollout.py:51-68): d_{-1} = 0^32,
+// d_j = SHA-256(d_{j-1} || LE-f64(round(h[jk:(j+1)k], 6))).  A chain is serial, so
+// each thread owns one rollout; it wins over the host (SHA-NI on every core) once a
+// batch has enough rollouts to fill the GPU's warps (DESIGN 5.6).  SHA-256 is FIPS
+// 180-4: the round constants are the first 32 bits of the fractional parts of the
+// cube roots of the first 64 primes (generated, and checked against hashlib).
+__constant__ uint32_t kSha256K[64] = {
+    0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u, 0x923f82a4u, 0xab1c5ed5u,
+    0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u, 0x72be5d74u, 0x80deb1feu, 0x9bdc06a7u, 0xc19bf174u,
+    0xe49b69c1u, 0xefbe4786u, 0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu, 0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau,
+    0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u, 0xc6e00bf3u, 0xd5a79147u, 0x06ca6351u, 0x14292967u,
+    0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu, 0x53380d13u, 0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u,
+    0xa2bfe8a1u, 0xa81a664bu, 0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u,
+    0x19a4c116u, 0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au, 0x5b9cca4fu, 0x682e6ff3u,
+    0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u, 0x90befffau, 0xa4506cebu, 0xbef9a3f7u, 0xc67178f2u};
+
+__device__ __forceinline__ uint32_t rotr32(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
+
+__device__ __forceinline__ void sha256_block(uint32_t (&st)[8], uint32_t (&w)[16]) {
+  uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
+#pragma unroll
+  for (int t = 0; t < 64; ++t) {
+    uint32_t wt;
+    if (t < 16) {
+      wt = w[t];
+    } else {
+      const uint32_t w15 = w[(t - 15) & 15], w2 = w[(t - 2) & 15];
+      const uint32_t s0 = rotr32(w15, 7) ^ rotr32(w15, 18) ^ (w15 >> 3);
+      const uint32_t s1 = rotr32(w2, 17) ^ rotr32(w2, 19) ^ (w2 >> 10);
+      wt = w[t & 15] = w[t & 15] + s0 + w[(t - 7) & 15] + s1;
+    }
+    const uint32_t t1 = h + (rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25)) + ((e & f) ^ (~e & g)) + kSha256K[t] + wt;
+    const uint32_t t2 = (rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22)) + ((a & b) ^ (a & c) ^ (b & c));
+    h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + t2;
+  }
+  st[0] += a; st[1] += b; st[2] += c; st[3] += d; st[4] += e; st[5] += f; st[6] += g; st[7] += h;
+}
+
+constexpr int kShaPrefetch = 8;  // 64-byte message blocks (8 float64) ahead
+
+__device__ __forceinline__ const void* elem_addr(const void* in, int dtype, int64_t i) {
+  const int size = dtype == 0 ? 8 : dtype == 1 ? 4 : 2;
+  return static_cast<const char*>(in) + i * size;
+}
+
+__device__ __forceinline__ double round6_value(double x) {
+  if (x != x) return __longlong_as_double(__double_as_longlong(x) | 0x0008000000000000ll);  // quiet, keep payload
+  return __ddiv_rn(rint(__dmul_rn(x, 1e6)), 1e6);
+}
+
+// One thread per rollout: ceil(T/k) digests (one for T = 0), 32 bytes each, at
+// digests_out + 32 * dig_off[r].  The message of digest j is the previous digest
+// (8 words) followed by the block's rounded float64 values, two big-endian words
+// each (the bytes of the little-endian double), then the SHA padding.  Word pairs of
+// block b map to "element" slots e = 8b - 4 + s (e < 0: the previous digest).
+__global__ void exact_chain_kernel(const void* __restrict__ in, int dtype, const int64_t* __restrict__ row_off,
+                                   int n_roll, int H, int k, const int64_t* __restrict__ dig_off,
+                                   uint8_t* __restrict__ digests_out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_roll) return;
+  const int64_t T = row_off[r + 1] - row_off[r];
+  const int64_t nd = T > 0 ? (T + k - 1) / k : 1;
+  uint32_t prev[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+  uint32_t* out = reinterpret_cast<uint32_t*>(digests_out + 32 * dig_off[r]);
+  for (int64_t j = 0; j < nd; ++j) {
+    const int64_t rows = T > 0 ? min((int64_t)k, T - j * k) : 0;
+    const int64_t base = (row_off[r] + j * k) * (int64_t)H;
+    const int64_t n_el = rows * (int64_t)H;
+    const int64_t n_blocks = (8 + 2 * n_el + 3 + 15) / 16;  // data words + 0x80 word + 64-bit length
+    const uint64_t bits = (uint64_t)(32 + 8 * n_el) * 8u;
+    uint32_t st[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
+                      0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
+    for (int64_t b = 0; b < n_blocks; ++b) {
+      // one thread per chain leaves little to hide load latency behind: pull the line
+      // kShaPrefetch blocks ahead into L1 so the element loads below hit it
+      if (8 * (b + kShaPrefetch) - 4 < n_el)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(elem_addr(in, dtype, base + 8 * (b + kShaPrefetch) - 4)));
+      uint32_t w[16];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int64_t e = 8 * b - 4 + s;
+        uint32_t lo = 0u, hi = 0u;
+        if (s < 4 && b == 0) {  // the previous digest
+          lo = prev[2 * s];
+          hi = prev[2 * s + 1];
+        } else if (e < n_el) {
+          const unsigned long long v =
+              (unsigned long long)__double_as_longlong(round6_value(load_as_f64(in, dtype, base + e)));
+          lo = __byte_perm((uint32_t)v, 0u, 0x0123);          // bytes 0..3 as a big-endian word
+          hi = __byte_perm((uint32_t)(v >> 32), 0u, 0x0123);  // bytes 4..7
+        } else if (e == n_el) {
+          lo = 0x80000000u;
+        }
+        w[2 * s] = lo;
+        w[2 * s + 1] = hi;
+      }
+      if (b == n_blocks - 1) {
+        w[14] = (uint32_t)(bits >> 32);
+        w[15] = (uint32_t)bits;
+      }
+      sha256_block(st, w);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      out[8 * j + q] = __byte_perm(st[q], 0u, 0x0123);  // big-endian digest bytes
+      prev[q] = st[q];
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------- synthetic input
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -1543,6 +1654,16 @@ int tl_partition_destroy(void** streams) {
 }
 
 int32_t tl_stream_sms(void* stream) { return stream_sms(static_cast<cudaStream_t>(stream)); }
+
+int tl_exact_chains(const void* hidden, int32_t dtype, const int64_t* row_off, int32_t n_roll, int32_t H, int32_t k,
+                    const int64_t* digest_off, uint8_t* digests_out, void* stream) {
+  if (n_roll < 0 || H < 0 || k < 1 || dtype < 0 || dtype > 3) return TL_EINVAL;  // H = 0: empty rows
+  if (n_roll == 0) return TL_OK;
+  if (!hidden || !row_off || !digest_off || !digests_out) return TL_EINVAL;
+  exact_chain_kernel<<<(n_roll + 31) / 32, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      hidden, dtype, row_off, n_roll, H, k, digest_off, digests_out);
+  return launch_status();
+}
 
 int tl_round6(const void* in, int32_t dtype, int64_t n, double* out, void* stream) {
   if (n < 0 || dtype < 0 || dtype > 3) return TL_EINVAL;

@@ -100,8 +100,56 @@ def _staging(dev, elems: int):
     return cur
 
 
+def build_commitments_device(hidden, row_offsets, k: int = 32) -> list[list[bytes]]:
+    """Exact-mode commitments with the whole SHA-256 chains on the GPU
+    (``tl_exact_chains``, one thread per rollout).  Byte-identical to
+    ``build_commitments`` per rollout.  Each chain is latency-bound (~18 MB/s per
+    thread), so the kernel time is flat in the rollout count: it beats host SHA-NI
+    on all cores only from ~2048 rollouts (``DEVICE_SHA_MIN_ROLLOUTS``)."""
+    if k < 1:
+        raise ValueError("interval must be >= 1")
+    if not torch.cuda.is_available():
+        raise RuntimeError("exact mode needs a CUDA device (no CPU fallback)")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if isinstance(hidden, torch.Tensor):
+        t = hidden
+    else:
+        a = np.ascontiguousarray(hidden)
+        t = torch.from_numpy(a if a.flags.writeable else a.copy())
+    if t.dim() != 2:
+        raise ValueError("hidden must be (rows, H)")
+    if t.dtype not in _DTYPE_CODE:
+        t = t.to(torch.float64)
+    t = t.to(dev).contiguous()
+    offs = np.asarray(row_offsets, dtype=np.int64)
+    n_rows, H = t.shape
+    if offs[0] != 0 or offs[-1] != n_rows or np.any(np.diff(offs) < 0):
+        raise ValueError("row_offsets must start at 0, be non-decreasing and end at n_rows")
+    R = len(offs) - 1
+    nd = np.maximum(1, -(-np.diff(offs) // k))
+    doff = np.concatenate([[0], np.cumsum(nd)]).astype(np.int64)
+    out = torch.empty((max(int(doff[-1]), 1), 32), dtype=torch.uint8, device=dev)
+    # keep the device copies referenced until the kernel is enqueued (a temporary's
+    # memory would be handed to the next allocation before the launch)
+    offs_dev = torch.from_numpy(offs).to(dev)
+    doff_dev = torch.from_numpy(doff[:-1].copy()).to(dev)
+    if t.numel() == 0:  # every rollout empty: the kernel reads no element, but wants a pointer
+        t = torch.zeros(1, dtype=t.dtype, device=dev)
+    rc = _ffi.load().tl_exact_chains(t.data_ptr(), _DTYPE_CODE[t.dtype], offs_dev.data_ptr(), R, H, k,
+                                     doff_dev.data_ptr(), out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+    _ffi.check(rc, "tl_exact_chains")
+    host = out.cpu().numpy()
+    return [[host[j].tobytes() for j in range(doff[r], doff[r + 1])] for r in range(R)]
+
+
+# Rollouts from which the GPU chains beat host SHA-NI on all cores
+# (tools/bench_exact.py --device-sweep, H=5120: 1024 -> host, 2048 -> 0.90 M vs 0.63 M
+# tokens/s, 4096 -> 1.77 M vs 0.64 M).
+DEVICE_SHA_MIN_ROLLOUTS = 2048
+
+
 def build_commitments_batch(hidden, row_offsets, k: int = 32, threads: int | None = None,
-                            group_rows: int = 65536) -> list[list[bytes]]:
+                            group_rows: int = 65536, sha: str = "auto") -> list[list[bytes]]:
     """Exact-mode commitments for many rollouts at once (the validator's batch form).
 
     ``hidden`` is a (sum T, H) tensor (device or host; bf16 / f16 / f32 / f64) and
@@ -111,6 +159,10 @@ def build_commitments_batch(hidden, row_offsets, k: int = 32, threads: int | Non
     serial-per-rollout SHA-256 chains of different rollouts run on all host cores
     while the next group is rounded and copied.  Byte-identical to
     ``build_commitments`` per rollout (rollout.py:51-68)."""
+    if sha not in ("auto", "host", "device"):
+        raise ValueError("sha must be 'auto', 'host' or 'device'")
+    if sha == "device" or (sha == "auto" and len(row_offsets) - 1 >= DEVICE_SHA_MIN_ROLLOUTS):
+        return build_commitments_device(hidden, row_offsets, k)
     if k < 1:
         raise ValueError("interval must be >= 1")
     if not torch.cuda.is_available():

@@ -80,3 +80,43 @@ def test_gpu_exact_batch_matches_reference_per_rollout():
     got = build_commitments_batch(hb, offs, 7, group_rows=64)
     want = [EO.build_commitments(hb.to(torch.float64).numpy()[offs[r]:offs[r + 1]], 7) for r in range(len(lens))]
     assert got == want
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32, torch.bfloat16, torch.float16])
+def test_device_sha_chains_equal_host_chains(dtype):
+    """tl_exact_chains (SHA-256 chains on the GPU, one thread per rollout) against the
+    host chains over the same rounded values: ragged rollouts, T = 0, T < k, T % k != 0,
+    odd H, NaN / inf / -0.0 and huge values."""
+    from paper_2505_07291_b200.exact import build_commitments_batch, build_commitments_device
+    rng = np.random.default_rng(3)
+    H = 37
+    lens = [0, 1, 31, 32, 33, 64, 95, 200, 0, 7]
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    x = rng.normal(size=(int(offs[-1]), H)) * 10.0 ** rng.integers(-8, 8, size=(int(offs[-1]), H))
+    x[3, :4] = [np.nan, -np.inf, -0.0, 1e300]
+    t = torch.from_numpy(x).to(dtype)
+    for k in (32, 5):
+        got = build_commitments_device(t, offs, k)
+        want = build_commitments_batch(t, offs, k, sha="host")
+        assert got == want, (dtype, k)
+        assert all(len(g) == max(1, -(-n // k)) for g, n in zip(got, lens))
+
+
+def test_device_sha_matches_reference_goldens():
+    from paper_2505_07291_b200.exact import build_commitments_device
+    for case in load_cases():
+        arr = regen_input(case)
+        a2 = np.asarray(arr, dtype=np.float64)
+        if a2.ndim != 2:
+            continue
+        got = build_commitments_device(a2, [0, a2.shape[0]], case["k"])[0]
+        assert [d.hex() for d in got] == case["digests"], case["name"]
+
+
+def test_device_sha_empty_rows_and_empty_batches():
+    """H = 0 (rows without values) and all-empty rollouts: digests over the chained
+    prefix only, exactly as the reference's hashlib chain."""
+    from paper_2505_07291_b200.exact import build_commitments_batch, build_commitments_device
+    for shape, offs in (((40, 0), [0, 33, 33, 40]), ((0, 5), [0, 0, 0])):
+        x = np.zeros(shape)
+        assert build_commitments_device(x, offs, 32) == build_commitments_batch(x, offs, 32, sha="host")

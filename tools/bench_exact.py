@@ -29,13 +29,45 @@ def _cpu_worker(args):
     q.put((time.perf_counter() - t0, len(d)))
 
 
+def device_sweep(H: int, T: int, rollouts) -> dict:
+    """Whole chains on the GPU (tl_exact_chains) vs the host-SHA path, by batch size."""
+    import numpy as np
+    import torch
+    from paper_2505_07291_b200.exact import build_commitments_batch, build_commitments_device
+    from paper_2505_07291_b200.synth import synth_device
+    res = {}
+    for R in rollouts:
+        x = synth_device(R * T, H, seed=5)
+        offs = np.arange(R + 1, dtype=np.int64) * T
+        build_commitments_device(x[:T], offs[:2], 32)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dev = build_commitments_device(x, offs, 32)
+        t_dev = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        host = build_commitments_batch(x, offs, 32, sha="host")
+        t_host = time.perf_counter() - t0
+        res[R] = {"device_s": t_dev, "host_s": t_host, "device_tokens_per_s": R * T / t_dev,
+                  "host_tokens_per_s": R * T / t_host, "equal": dev == host}
+        del x
+        torch.cuda.empty_cache()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rollouts", type=int, default=32)
     ap.add_argument("--tokens", type=int, default=8192)
     ap.add_argument("--hidden", type=int, default=5120)
     ap.add_argument("--cpu-workers", type=int, default=0)
+    ap.add_argument("--device-sweep", default="", help="comma-separated rollout counts: GPU chains vs host SHA")
     args = ap.parse_args()
+    if args.device_sweep:
+        print(json.dumps({"mode": "exact, GPU SHA chains vs host SHA", "hidden": args.hidden,
+                          "tokens_per_rollout": args.tokens,
+                          "by_rollouts": device_sweep(args.hidden, args.tokens,
+                                                      [int(v) for v in args.device_sweep.split(",")])}))
+        return
     import numpy as np
     import torch
     from paper_2505_07291_b200.exact import build_commitments_batch
