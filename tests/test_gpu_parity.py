@@ -231,6 +231,50 @@ def test_verify_variants_match_oracle(H):
             check_verify_against_oracle(vb, offs, pf, th)
 
 
+def _adversarial_chunk(name: str, H: int, C: int = 32) -> np.ndarray:
+    """One chunk's (C, H) bits built to defeat threshold speculation (tools/bench_adversarial.py)."""
+    n = C * H
+    i = np.arange(n, dtype=np.int64)
+    rng = np.random.default_rng(5)
+    if name == "ascending_narrow_span":
+        b = 0x3F80 + (i * 127) // n
+    elif name == "ascending_wide_span":
+        b = (i * 0x7F7F) // n
+    elif name == "ascending_alternating_sign":
+        b = ((i * 0x7F7F) // n) | ((i & 1) << 15)
+    elif name == "descending_wide_span":
+        b = ((n - 1 - i) * 0x7F7F) // n
+    elif name == "spikes_in_zeros":
+        b = np.zeros(n, dtype=np.int64)
+        b[rng.choice(n, 128, replace=False)] = 0x4300
+    elif name == "three_values":
+        b = rng.choice(np.array([0x3F80, 0xBF80, 0x4000]), n)
+    elif name == "fp8_e4m3_ties":
+        t = torch.from_numpy(synth_bits(0, C, H, seed=4).view(np.int16)).view(torch.bfloat16)
+        return bits_np(t.float().to(torch.float8_e4m3fn).to(torch.bfloat16))
+    else:
+        raise ValueError(name)
+    return b.astype(np.uint16).reshape(C, H)
+
+
+@pytest.mark.parametrize("name", ["ascending_narrow_span", "ascending_wide_span", "ascending_alternating_sign",
+                                  "descending_wide_span", "spikes_in_zeros", "three_values", "fp8_e4m3_ties"])
+@pytest.mark.parametrize("H", [1024, 5120])
+def test_adversarial_orderings_match_oracle(name, H):
+    """Inputs that defeat the threshold speculation (every element beats the running
+    threshold, key spans beyond the 32-bit ranking keys, heavy ties) prove and verify
+    bit-exactly; whole chunks and a ragged tail, after a normal chunk so the carried
+    speculation is wrong for them."""
+    pat = _adversarial_chunk(name, H)
+    bits = np.concatenate([synth_bits(0, 32, H, seed=3), pat, pat, pat[:17]])
+    offs = [0, 64, 96, 113]
+    _, proofs = check_prove_against_oracle(bits, offs)
+    check_verify_against_oracle(bits, offs, proofs)
+    e5m2 = bits_np(torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).float()
+                   .to(torch.float8_e5m2).to(torch.bfloat16))
+    check_verify_against_oracle(e5m2, offs, proofs)
+
+
 def test_verify_identical_accepts_and_wrong_rejects():
     offs = [0, 128, 256]
     bits = synth_bits(0, 256, 1024, seed=1, dist=0)
