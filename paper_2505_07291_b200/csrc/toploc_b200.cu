@@ -1080,51 +1080,69 @@ __global__ void __launch_bounds__(kRecThreads) record_checks_kernel(const double
 }
 
 // ----------------------------------------------------------------------------- exact mode
+// dtype codes: 0 float64, 1 float32, 2 bfloat16, 3 float16
+template <int DT>
+__device__ __forceinline__ uint64_t load_raw(const void* in, int64_t i) {
+  if (DT == 0) return (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(in) + i);
+  if (DT == 1) return (uint64_t)__ldg(reinterpret_cast<const unsigned int*>(in) + i);
+  return (uint64_t)__ldg(reinterpret_cast<const unsigned short*>(in) + i);
+}
+
+// Widen a raw element to float64 exactly; NaNs keep sign and payload (quieted) the way
+// x86 cvtss2sd / numpy widen them.
+template <int DT>
+__device__ __forceinline__ double raw_to_f64(uint64_t raw) {
+  if (DT == 0) return __longlong_as_double((long long)raw);
+  if (DT == 1 || DT == 2) {
+    const uint32_t b = DT == 1 ? (uint32_t)raw : (uint32_t)raw << 16;
+    if ((b & 0x7FFFFFFFu) > 0x7F800000u)
+      return __longlong_as_double((long long)(((uint64_t)(b >> 31) << 63) | 0x7FF8000000000000ull |
+                                              ((uint64_t)(b & 0x7FFFFFu) << 29)));
+    return (double)__uint_as_float(b);
+  }
+  const uint16_t h = (uint16_t)raw;
+  if ((h & 0x7FFFu) > 0x7C00u)
+    return __longlong_as_double((long long)(((uint64_t)(h >> 15) << 63) | 0x7FF8000000000000ull |
+                                            ((uint64_t)(h & 0x3FFu) << 42)));
+  return (double)__half2float(__ushort_as_half(h));
+}
+
 __device__ __forceinline__ double load_as_f64(const void* in, int dtype, int64_t i) {
   switch (dtype) {
-    case 0: return reinterpret_cast<const double*>(in)[i];
-    case 1: {
-      const uint32_t b = reinterpret_cast<const uint32_t*>(in)[i];
-      if ((b & 0x7FFFFFFFu) > 0x7F800000u)  // NaN: widen payload like x86 cvtss2sd
-        return __longlong_as_double((long long)(((uint64_t)(b >> 31) << 63) | 0x7FF8000000000000ull |
-                                                ((uint64_t)(b & 0x7FFFFFu) << 29)));
-      return (double)__uint_as_float(b);
-    }
-    case 2: {
-      const uint32_t b = (uint32_t)reinterpret_cast<const uint16_t*>(in)[i] << 16;
-      if ((b & 0x7FFFFFFFu) > 0x7F800000u)
-        return __longlong_as_double((long long)(((uint64_t)(b >> 31) << 63) | 0x7FF8000000000000ull |
-                                                ((uint64_t)(b & 0x7FFFFFu) << 29)));
-      return (double)__uint_as_float(b);
-    }
-    default: {
-      const uint16_t h = reinterpret_cast<const uint16_t*>(in)[i];
-      if ((h & 0x7FFFu) > 0x7C00u)
-        return __longlong_as_double((long long)(((uint64_t)(h >> 15) << 63) | 0x7FF8000000000000ull |
-                                                ((uint64_t)(h & 0x3FFu) << 42)));
-      return (double)__half2float(__ushort_as_half(h));
-    }
+    case 0: return raw_to_f64<0>(load_raw<0>(in, i));
+    case 1: return raw_to_f64<1>(load_raw<1>(in, i));
+    case 2: return raw_to_f64<2>(load_raw<2>(in, i));
+    default: return raw_to_f64<3>(load_raw<3>(in, i));
   }
 }
 
+// np.round(x, 6) = rint(x * 1e6) / 1e6 in float64, the division correctly rounded.
+// The division is branch-free (no __ddiv_rn slow path) so it interleaves with the
+// SHA rounds of the chain kernel: q0 = RN(r * RN(1e-6)) is within 1.5 ulp of r/1e6,
+// the FMA remainder r - 1e6*q0 is exact, and q = RN(q0 + rem * RN(1e-6)) differs from
+// r/1e6 by < 2^-52 ulp.  r is an integer-valued double, so r/1e6 = N/15625 ulp units
+// for an integer N: it is never a rounding midpoint and never closer to one than
+// 1/31250 ulp, hence q = RN(r/1e6) exactly (tests/test_gpu_exact.py checks every
+// float32 input against torch's correctly rounded division).  0 keeps its sign, inf
+// stays inf; NaN keeps its payload, quieted (np.round).
+__device__ __forceinline__ double round6_value(double x) {
+  const double r = rint(__dmul_rn(x, 1e6));
+  const double q0 = __dmul_rn(r, 1e-6);
+  const double q = __fma_rn(__fma_rn(-q0, 1e6, r), 1e-6, q0);
+  const double nanq = __longlong_as_double(__double_as_longlong(x) | 0x0008000000000000ll);
+  return x != x ? nanq : (r == 0.0 || fabs(r) == __longlong_as_double(0x7FF0000000000000ll)) ? r : q;
+}
+
 __global__ void round6_kernel(const void* __restrict__ in, int dtype, int64_t n, double* __restrict__ out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double x = load_as_f64(in, dtype, i);
-    double r;
-    if (x != x) {  // np.round keeps (and quiets) the NaN payload
-      r = __longlong_as_double(__double_as_longlong(x) | 0x0008000000000000ll);
-    } else {
-      r = __ddiv_rn(rint(__dmul_rn(x, 1e6)), 1e6);
-    }
-    out[i] = r;
-  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = round6_value(load_as_f64(in, dtype, i));
 }
 
 // ----------------------------------------------------------------------------- exact mode on the GPU
 // The reference's commitment chain (rollout.py:51-68): d_{-1} = 0^32,
 // d_j = SHA-256(d_{j-1} || LE-f64(round(h[jk:(j+1)k], 6))).  A chain is serial, so
 // each thread owns one rollout; it wins over the host (SHA-NI on every core) once a
-// batch has enough rollouts to fill the GPU's warps (DESIGN 5.6).  SHA-256 is FIPS
+// batch has enough rollouts (DESIGN 5.6).  SHA-256 is FIPS
 // 180-4: the round constants are the first 32 bits of the fractional parts of the
 // cube roots of the first 64 primes (generated, and checked against hashlib).
 __constant__ uint32_t kSha256K[64] = {
@@ -1159,24 +1177,59 @@ __device__ __forceinline__ void sha256_block(uint32_t (&st)[8], uint32_t (&w)[16
   st[0] += a; st[1] += b; st[2] += c; st[3] += d; st[4] += e; st[5] += f; st[6] += g; st[7] += h;
 }
 
-constexpr int kShaPrefetch = 8;  // 64-byte message blocks (8 float64) ahead
+constexpr int kShaPrefetch = 16;  // 64-byte message blocks ahead (L1 line prefetch)
 
-__device__ __forceinline__ const void* elem_addr(const void* in, int dtype, int64_t i) {
-  const int size = dtype == 0 ? 8 : dtype == 1 ? 4 : 2;
-  return static_cast<const char*>(in) + i * size;
+template <int DT>
+__device__ __forceinline__ const void* elem_addr(const void* in, int64_t i) {
+  return static_cast<const char*>(in) + i * (DT == 0 ? 8 : DT == 1 ? 4 : 2);
 }
 
-__device__ __forceinline__ double round6_value(double x) {
-  if (x != x) return __longlong_as_double(__double_as_longlong(x) | 0x0008000000000000ll);  // quiet, keep payload
-  return __ddiv_rn(rint(__dmul_rn(x, 1e6)), 1e6);
+// Raw elements of message block b (element slots e = 8b - 4 + s; 0 outside the data).
+template <int DT>
+__device__ __forceinline__ void fetch_block(const void* in, int64_t base, int64_t n_el, int64_t b, uint64_t (&raw)[8]) {
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int64_t e = 8 * b - 4 + s;
+    raw[s] = (e >= 0 && e < n_el) ? load_raw<DT>(in, base + e) : 0ull;
+  }
 }
 
-// One thread per rollout: ceil(T/k) digests (one for T = 0), 32 bytes each, at
-// digests_out + 32 * dig_off[r].  The message of digest j is the previous digest
-// (8 words) followed by the block's rounded float64 values, two big-endian words
-// each (the bytes of the little-endian double), then the SHA padding.  Word pairs of
-// block b map to "element" slots e = 8b - 4 + s (e < 0: the previous digest).
-__global__ void exact_chain_kernel(const void* __restrict__ in, int dtype, const int64_t* __restrict__ row_off,
+// Message words of block b: the previous digest (block 0), the rounded values as the
+// big-endian words of their little-endian bytes, the 0x80 terminator, the bit length.
+template <int DT>
+__device__ __forceinline__ void assemble_block(const uint64_t (&raw)[8], int64_t b, int64_t n_el, int64_t n_blocks,
+                                               uint64_t bits, const uint32_t (&prev)[8], uint32_t (&w)[16]) {
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int64_t e = 8 * b - 4 + s;
+    uint32_t lo = 0u, hi = 0u;
+    if (e < 0) {
+      lo = prev[2 * s];
+      hi = prev[2 * s + 1];
+    } else if (e < n_el) {
+      const uint64_t v = (uint64_t)__double_as_longlong(round6_value(raw_to_f64<DT>(raw[s])));
+      lo = __byte_perm((uint32_t)v, 0u, 0x0123);
+      hi = __byte_perm((uint32_t)(v >> 32), 0u, 0x0123);
+    } else if (e == n_el) {
+      lo = 0x80000000u;
+    }
+    w[2 * s] = lo;
+    w[2 * s + 1] = hi;
+  }
+  if (b == n_blocks - 1) {
+    w[14] = (uint32_t)(bits >> 32);
+    w[15] = (uint32_t)bits;
+  }
+}
+
+// The reference's commitment chain (rollout.py:51-68), one thread per rollout:
+// ceil(T/k) digests (one for T = 0), 32 bytes each, at digests_out + 32 * dig_off[r].
+// The message of digest j is the previous digest (8 words) followed by the block's
+// rounded float64 values, then the SHA padding.  A chain is serial and one thread has
+// nothing to hide latency behind but its own work, so the loop is software-pipelined:
+// block b+2's loads are issued and block b+1 is rounded before block b is compressed.
+template <int DT>
+__global__ void exact_chain_kernel(const void* __restrict__ in, const int64_t* __restrict__ row_off,
                                    int n_roll, int H, int k, const int64_t* __restrict__ dig_off,
                                    uint8_t* __restrict__ digests_out) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1193,35 +1246,21 @@ __global__ void exact_chain_kernel(const void* __restrict__ in, int dtype, const
     const uint64_t bits = (uint64_t)(32 + 8 * n_el) * 8u;
     uint32_t st[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
                       0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
+    uint64_t ra[8], rb[8];
+    uint32_t w[16], wn[16];
+    fetch_block<DT>(in, base, n_el, 0, ra);
+    assemble_block<DT>(ra, 0, n_el, n_blocks, bits, prev, w);
+    fetch_block<DT>(in, base, n_el, 1, ra);
     for (int64_t b = 0; b < n_blocks; ++b) {
-      // one thread per chain leaves little to hide load latency behind: pull the line
-      // kShaPrefetch blocks ahead into L1 so the element loads below hit it
       if (8 * (b + kShaPrefetch) - 4 < n_el)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(elem_addr(in, dtype, base + 8 * (b + kShaPrefetch) - 4)));
-      uint32_t w[16];
-#pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        const int64_t e = 8 * b - 4 + s;
-        uint32_t lo = 0u, hi = 0u;
-        if (s < 4 && b == 0) {  // the previous digest
-          lo = prev[2 * s];
-          hi = prev[2 * s + 1];
-        } else if (e < n_el) {
-          const unsigned long long v =
-              (unsigned long long)__double_as_longlong(round6_value(load_as_f64(in, dtype, base + e)));
-          lo = __byte_perm((uint32_t)v, 0u, 0x0123);          // bytes 0..3 as a big-endian word
-          hi = __byte_perm((uint32_t)(v >> 32), 0u, 0x0123);  // bytes 4..7
-        } else if (e == n_el) {
-          lo = 0x80000000u;
-        }
-        w[2 * s] = lo;
-        w[2 * s + 1] = hi;
-      }
-      if (b == n_blocks - 1) {
-        w[14] = (uint32_t)(bits >> 32);
-        w[15] = (uint32_t)bits;
-      }
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(elem_addr<DT>(in, base + 8 * (b + kShaPrefetch) - 4)));
+      fetch_block<DT>(in, base, n_el, b + 2, rb);
+      assemble_block<DT>(ra, b + 1, n_el, n_blocks, bits, prev, wn);
       sha256_block(st, w);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) w[q] = wn[q];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ra[q] = rb[q];
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -1660,8 +1699,14 @@ int tl_exact_chains(const void* hidden, int32_t dtype, const int64_t* row_off, i
   if (n_roll < 0 || H < 0 || k < 1 || dtype < 0 || dtype > 3) return TL_EINVAL;  // H = 0: empty rows
   if (n_roll == 0) return TL_OK;
   if (!hidden || !row_off || !digest_off || !digests_out) return TL_EINVAL;
-  exact_chain_kernel<<<(n_roll + 31) / 32, 32, 0, static_cast<cudaStream_t>(stream)>>>(
-      hidden, dtype, row_off, n_roll, H, k, digest_off, digests_out);
+  const dim3 grid((n_roll + 31) / 32), block(32);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (dtype) {
+    case 0: exact_chain_kernel<0><<<grid, block, 0, st>>>(hidden, row_off, n_roll, H, k, digest_off, digests_out); break;
+    case 1: exact_chain_kernel<1><<<grid, block, 0, st>>>(hidden, row_off, n_roll, H, k, digest_off, digests_out); break;
+    case 2: exact_chain_kernel<2><<<grid, block, 0, st>>>(hidden, row_off, n_roll, H, k, digest_off, digests_out); break;
+    default: exact_chain_kernel<3><<<grid, block, 0, st>>>(hidden, row_off, n_roll, H, k, digest_off, digests_out); break;
+  }
   return launch_status();
 }
 

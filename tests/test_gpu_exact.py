@@ -37,6 +37,51 @@ def test_gpu_round6_bitwise_equals_numpy():
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
 
 
+def test_gpu_round6_every_float32():
+    """The branch-free division in round6_value (csrc, FMA-corrected reciprocal) against
+    a correctly rounded division, for every float32 bit pattern (which includes every
+    bfloat16 and float16 value).  The reference side is rint(x * 1e6) / 1e6 in float64
+    on the GPU (IEEE division), itself checked against numpy on a sample."""
+    sample = np.random.default_rng(7).integers(0, 1 << 32, size=1 << 16, dtype=np.uint64).astype(np.uint32)
+    xs = sample.view(np.float32).astype(np.float64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        ref_np = np.round(xs, 6)
+    tx = torch.from_numpy(xs).cuda()
+    # a tensor divisor: torch turns division by a Python scalar into a reciprocal multiply
+    ref_t = (torch.round(tx * 1e6) / torch.full_like(tx, 1e6)).cpu().numpy()
+    fin = np.isfinite(xs)
+    assert np.array_equal(ref_np[fin].view(np.uint64), ref_t[fin].view(np.uint64))
+    step = 1 << 28
+    for start in range(0, 1 << 32, step):
+        v = torch.arange(start, start + step, dtype=torch.int64, device="cuda")
+        x = torch.where(v >= (1 << 31), v - (1 << 32), v).to(torch.int32).view(torch.float32)
+        got = round6_device(x)
+        xd = x.double()
+        want = torch.round(xd * 1e6) / torch.full_like(xd, 1e6)
+        nan = torch.isnan(x)
+        same = (got.view(torch.int64) == want.view(torch.int64)) | nan
+        assert bool(same.all()), f"slice {start:#x}: first mismatch at {int((~same).nonzero()[0]) + start:#x}"
+        assert bool(torch.isnan(got[nan]).all())
+        del v, x, xd, got, want, nan, same
+
+
+def test_gpu_round6_random_float64_bit_patterns():
+    """Random float64 bit patterns over the whole exponent range, and values a few ulps
+    from multiples of 1e-6 (the hardest quotients), against numpy."""
+    rng = np.random.default_rng(11)
+    bits = rng.integers(0, 1 << 63, size=1 << 22, dtype=np.int64).astype(np.uint64)
+    bits |= rng.integers(0, 2, size=bits.size, dtype=np.uint64) << np.uint64(63)
+    x = bits.view(np.float64)
+    near = (rng.integers(-10**12, 10**12, size=1 << 20) / 1e6).astype(np.float64)
+    near = np.nextafter(near, np.where(rng.integers(0, 2, size=near.size) == 1, np.inf, -np.inf))
+    x = np.concatenate([x, near, near * 0.5 + 0.5e-6])
+    with np.errstate(over="ignore", invalid="ignore"):
+        want = np.round(x, 6)
+    got = round6_device(x).cpu().numpy()
+    ok = (got.view(np.uint64) == want.view(np.uint64)) | np.isnan(x)
+    assert ok.all(), x[~ok][:5]
+
+
 def test_gpu_round6_from_bf16_f32_f16():
     rng = np.random.default_rng(1)
     x = torch.from_numpy(rng.normal(size=(64, 33)).astype(np.float32))

@@ -40,6 +40,8 @@ def device_sweep(H: int, T: int, rollouts) -> dict:
         x = synth_device(R * T, H, seed=5)
         offs = np.arange(R + 1, dtype=np.int64) * T
         build_commitments_device(x[:T], offs[:2], 32)  # warm-up
+        nw = min(R, max(1, 65536 // T))  # one full row group: allocates and pins the host staging
+        build_commitments_batch(x[:nw * T], offs[:nw + 1], 32, sha="host")
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         dev = build_commitments_device(x, offs, 32)
