@@ -35,6 +35,11 @@ CONFIGS = {
 CHUNK, TOPK = 32, 128
 PROOF_BYTES = 2 + 2 * TOPK
 JITTER_THR = 3277          # 5 % of elements +-1 ulp in the validator's recompute
+# --schedule auto: the partitioned pipeline from this many chunks per GPU, one CUDA graph per
+# step below.  Measured: configuration 1 (64 chunks, H 1024) graph 0.080 ms vs partition
+# 0.115 ms; H 5120 at 256 / 1024 / 4096 / 16384 chunks partition 0.123 / 0.179 / 0.440 /
+# 1.534 ms vs graph 0.174 / 0.224 / 0.554 / 1.884 ms.
+AUTO_PIPELINE_MIN_CHUNKS = 256
 LAUNCHES_PER_STEP = 7      # select: prefix+select; commit: inv_table+commit; verify: prefix+verify+verdict
 
 
@@ -265,6 +270,10 @@ def run_b200(args, cfg, rank, world, local_rank):
             okp.append(pr[0] == got[j].tobytes())
         spot = {"chunks": js, "proofs_bit_exact": all(okp)}
 
+    if args.schedule == "auto":
+        # small batches are latency-bound: one CUDA graph per step beats the pipelines
+        args.schedule = "partition" if plan.n_chunks >= AUTO_PIPELINE_MIN_CHUNKS else "graph"
+    args.pipeline_on = args.schedule in ("pipeline", "partition")
     pipe = None
     if args.schedule == "partition":
         try:
@@ -489,14 +498,16 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--dist", default="normal", choices=["normal", "massive"])
+    ap.add_argument("--rollouts", type=int, default=0, help="override the configuration's rollout count (sweeps)")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--e2e-rollouts", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-tokens", type=int, default=8192)
     ap.add_argument("--no-spot-check", dest="spot_check", action="store_false")
-    ap.add_argument("--schedule", default="partition", choices=["partition", "pipeline", "serial", "graph"],
-                    help="partition (default): the pipeline on two SM partitions (green contexts), commit on "
+    ap.add_argument("--schedule", default="auto", choices=["auto", "partition", "pipeline", "serial", "graph"],
+                    help="auto (default): partition from 256 chunks per GPU (AUTO_PIPELINE_MIN_CHUNKS), graph below; "
+                         "partition: the pipeline on two SM partitions (green contexts), commit on "
                          "--commit-sms SMs, select/verify on the rest; "
                          "pipeline: commit(k) on a side stream, co-resident with verify(k-1) and select(k+1); "
                          "serial: tl_select, tl_commit, tl_verify back to back; graph: the serial step "
@@ -518,7 +529,10 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.rollouts:
+        cfg["R"] = args.rollouts
+        cfg["name"] = f"{cfg['name']} (rollouts overridden: {args.rollouts})"
     if args.impl == "reference":     # rank 0 alone times the CPU path; other ranks exit 0
         run_reference(args, cfg, rank, world)
         return

@@ -1447,10 +1447,16 @@ int launch_commit_t(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, 
 
 // co_resident = 0: 32 warps, full 128 KiB table (fastest alone); 1: 8 warps, 64 KiB
 // half table, <= 64 registers -- fits beside 16 one-warp select/verify CTAs per SM.
+// A batch with at most one chunk per SM sub-partition runs 4-warp CTAs instead: every
+// chunk's warp then has a sub-partition to itself and the call is one chunk's latency
+// (a 32-warp CTA would stack 8 chunks on each sub-partition of a few SMs).
+constexpr int kSmallCommitWarps = 4;
 int launch_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, const uint16_t* tables,
                   uint8_t* proofs, unsigned long long* next, int co_resident, cudaStream_t st) {
-  return co_resident ? launch_commit_t<kCoCommitWarps, true>(idx, bits, n_chunks, K, tables, proofs, next, st)
-                     : launch_commit_t<kCommitWarps, false>(idx, bits, n_chunks, K, tables, proofs, next, st);
+  if (co_resident) return launch_commit_t<kCoCommitWarps, true>(idx, bits, n_chunks, K, tables, proofs, next, st);
+  if (n_chunks <= (int64_t)stream_sms(st) * kSmallCommitWarps)
+    return launch_commit_t<kSmallCommitWarps, false>(idx, bits, n_chunks, K, tables, proofs, next, st);
+  return launch_commit_t<kCommitWarps, false>(idx, bits, n_chunks, K, tables, proofs, next, st);
 }
 
 }  // namespace
