@@ -139,21 +139,42 @@ def _cpu_worker(args):
     q.put(("done", (dt, T, bool(verdict[0]))))
 
 
-def cpu_sample(T: int, H: int, workers: int, steps: int = 1, warmup: int = 0):
+def _cpu_exact_worker(args):
+    """One worker = one rollout slice through the reference's own exact-mode algorithm
+    (oracle/exact_oracle.py restates rollout.py:51-68): commitments from the prover's
+    states, then the validator's recompute and digest-list compare (checks.py:209-213)."""
+    (T, H, seed, start_evt, q) = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    import numpy as np
+    from oracle import exact_oracle as EO
+    from oracle.synth_cpu import synth_bits
+    bits = np.concatenate([synth_bits(r, min(512, T - r), H, seed) for r in range(0, T, 512)])
+    hidden = (bits.astype(np.uint32) << 16).view(np.float32)
+    q.put(("ready", None))
+    start_evt.wait()
+    t0 = time.perf_counter()
+    claimed = EO.build_commitments(hidden, CHUNK)
+    ok = EO.build_commitments(hidden, CHUNK) == claimed
+    dt = time.perf_counter() - t0
+    q.put(("done", (dt, T, ok)))
+
+
+def cpu_sample(T: int, H: int, workers: int, steps: int = 1, warmup: int = 0, worker=None):
     """Run `warmup + steps` rounds of `workers` parallel oracle prove+verify slices."""
     ctx = mp.get_context("spawn")
     results = []
     for it in range(warmup + steps):
         q = ctx.Queue()
         evt = ctx.Event()
-        procs = [ctx.Process(target=_cpu_worker, args=((T, H, 7 + it * 1000 + w, evt, q),)) for w in range(workers)]
+        procs = [ctx.Process(target=worker or _cpu_worker, args=((T, H, 7 + it * 1000 + w, evt, q),))
+                 for w in range(workers)]
         for p in procs:
             p.start()
-        for _ in procs:
-            assert q.get()[0] == "ready"
+        for _ in procs:  # a worker that dies raises queue.Empty here instead of hanging the bench
+            assert q.get(timeout=600)[0] == "ready"
         t0 = time.perf_counter()
         evt.set()
-        done = [q.get()[1] for _ in procs]
+        done = [q.get(timeout=1800)[1] for _ in procs]
         wall = time.perf_counter() - t0
         for p in procs:
             p.join()
@@ -194,6 +215,12 @@ def run_reference(args, cfg, rank, world):
         "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "all_accepted": ok,
     }
+    # the reference's own exact-mode path (rollout.py:51-68 + checks.py:209-213) on the same cores
+    etps, ewall, eok = cpu_sample(T_slice, cfg["H"], workers, steps=1, warmup=0, worker=_cpu_exact_worker)
+    line["cpu_baseline"]["reference_exact_mode"] = {
+        "value": etps, "unit": "tokens/s", "cores": workers, "digests_match": eok,
+        "sample": f"{workers} x {T_slice}-token slices: build_commitments + recompute-and-compare "
+                  "(oracle/exact_oracle.py)"}
     print(json.dumps(line), flush=True)
 
 
@@ -444,6 +471,12 @@ def run_b200(args, cfg, rank, world, local_rank):
         cpu = {"value": tps, "unit": "tokens/s", "cores": workers, "kind": "port",
                "sample": f"{workers} parallel {args.cpu_tokens}-token slices x H={H} "
                          f"(oracle/toploc_oracle.py prove+verify, one process per core), wall {wall:.1f}s"}
+        # the reference's own (exact-mode) path on the same cores, for scale
+        etps, ewall, eok = cpu_sample(1024, H, workers, steps=1, warmup=0, worker=_cpu_exact_worker)
+        cpu["reference_exact_mode"] = {
+            "value": etps, "unit": "tokens/s", "cores": workers, "per_core": etps / workers, "digests_match": eok,
+            "sample": f"{workers} parallel 1024-token slices x H={H}: build_commitments + recompute-and-compare "
+                      f"(oracle/exact_oracle.py, the reference's rollout.py:51-68), wall {ewall:.1f}s"}
 
     if rank == 0:
         line = {
