@@ -202,9 +202,13 @@ class ToplocEngine:
         return self._ws
 
     def _workspace_used(self) -> None:
+        cur = torch.cuda.current_stream(self.device)
         ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(self.device))
+        ev.record(cur)
         self._ws_done = ev
+        # if a later call grows the workspace, the allocator must not hand this block out
+        # again before the work queued here on another stream has finished
+        self._ws.record_stream(cur)
 
     def _offsets(self, offs: np.ndarray):
         co = np.zeros(len(offs), dtype=np.int64)
