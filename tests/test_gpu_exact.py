@@ -165,3 +165,27 @@ def test_device_sha_empty_rows_and_empty_batches():
     for shape, offs in (((40, 0), [0, 33, 33, 40]), ((0, 5), [0, 0, 0])):
         x = np.zeros(shape)
         assert build_commitments_device(x, offs, 32) == build_commitments_batch(x, offs, 32, sha="host")
+
+
+def test_batch_auto_switches_to_device_chains_at_threshold(monkeypatch):
+    """sha="auto" hashes on the GPU from DEVICE_SHA_MIN_ROLLOUTS rollouts and on the host
+    below; both give the reference's digests."""
+    from paper_2505_07291_b200 import exact
+    from oracle import exact_oracle as EO
+    rng = np.random.default_rng(9)
+    R = exact.DEVICE_SHA_MIN_ROLLOUTS
+    lens = rng.integers(0, 70, size=R)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    h = torch.from_numpy(rng.normal(size=(int(offs[-1]), 12)).astype(np.float32)).to(torch.bfloat16)
+    used = []
+    real = exact.build_commitments_device
+    monkeypatch.setattr(exact, "build_commitments_device", lambda *a, **k: used.append(1) or real(*a, **k))
+    big = exact.build_commitments_batch(h.cuda(), offs, 32)
+    assert used, "auto did not take the GPU chains at the threshold"
+    n_small = R // 2
+    small = exact.build_commitments_batch(h[:offs[n_small]].cuda(), offs[:n_small + 1], 32)
+    assert len(used) == 1, "auto took the GPU chains below the threshold"
+    h64 = h.to(torch.float64).numpy()
+    for r in list(range(8)) + [R - 1]:
+        assert big[r] == EO.build_commitments(h64[offs[r]:offs[r + 1]], 32)
+    assert small == big[:n_small]
