@@ -200,8 +200,10 @@ int tl_round6(const void* in, int32_t dtype, int64_t n, double* out, void* strea
  * tl_round6, rows delimited by row_off, device int64 [n_roll+1]), the reference's
  * commitment chain d_j = SHA-256(d_{j-1} || LE-f64(round(block_j, 6))) over k-row
  * blocks (one digest for T = 0).  digest_off (device int64 [n_roll]) gives each
- * rollout's first digest; digests_out receives 32 bytes per digest.  One thread per
- * rollout: faster than host SHA once a batch has many rollouts.
+ * rollout's first digest; digests_out receives 32 bytes per digest.  One lane per
+ * rollout (a producer warp packs the message blocks, a SHA warp compresses them):
+ * faster than host SHA-NI on all cores from ~700 rollouts.  Replaces
+ * swarm/worker/rollout.py:51-68 (build_commitments) for a batch of rollouts.
  */
 int tl_exact_chains(const void* hidden, int32_t dtype, const int64_t* row_off, int32_t n_roll,
                     int32_t H, int32_t k, const int64_t* digest_off, uint8_t* digests_out,

@@ -1253,50 +1253,121 @@ __device__ __forceinline__ void assemble_block(const uint64_t (&raw)[8], int64_t
   }
 }
 
-// The reference's commitment chain (rollout.py:51-68), one thread per rollout:
+// Position of one rollout's chain: digest j, message block b of that digest.
+struct ChainCursor {
+  int64_t T, row0, j, b, nd, n_el, n_blocks, base;
+  int H, k;
+  __device__ __forceinline__ void start_digest() {
+    const int64_t rows = T > 0 ? min((int64_t)k, T - j * k) : 0;
+    base = (row0 + j * k) * (int64_t)H;
+    n_el = rows * (int64_t)H;
+    n_blocks = (8 + 2 * n_el + 3 + 15) / 16;  // data words + 0x80 word + 64-bit length
+  }
+  __device__ __forceinline__ void init(int64_t T_, int64_t row0_, int H_, int k_) {
+    T = T_; row0 = row0_; H = H_; k = k_; j = 0; b = 0;
+    nd = T > 0 ? (T + k - 1) / k : 1;
+    start_digest();
+  }
+  __device__ __forceinline__ uint64_t bits() const { return (uint64_t)(32 + 8 * n_el) * 8u; }
+  __device__ __forceinline__ void advance() {
+    if (++b == n_blocks) {
+      b = 0;
+      if (++j < nd) start_digest();
+    }
+  }
+  // message blocks over the whole chain
+  __device__ __forceinline__ int64_t total_blocks() const {
+    auto nb = [](int64_t n) { return (8 + 2 * n + 3 + 15) / 16; };
+    if (T <= 0) return nb(0);
+    const int64_t rem = T % k;
+    return (T / k) * nb((int64_t)k * H) + (rem ? nb(rem * H) : 0);
+  }
+};
+
+constexpr int kChainStages = 4;  // message blocks in flight between the two warps
+
+__device__ __forceinline__ void named_bar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void named_bar_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+
+// The reference's commitment chain (rollout.py:51-68), one chain per rollout:
 // ceil(T/k) digests (one for T = 0), 32 bytes each, at digests_out + 32 * dig_off[r].
 // The message of digest j is the previous digest (8 words) followed by the block's
-// rounded float64 values, then the SHA padding.  A chain is serial and one thread has
-// nothing to hide latency behind but its own work, so the loop is software-pipelined:
-// block b+2's loads are issued and block b+1 is rounded before block b is compressed.
+// rounded float64 values, then the SHA padding.
+//
+// A chain is serial, so the only parallelism is one lane per rollout, and a B200 sees
+// ~one warp per SM sub-partition: the compression is latency-bound on its own
+// dependencies.  The CTA is therefore warp-specialised over 32 rollouts: warp 1 loads,
+// rounds and packs the message blocks into a shared-memory ring (kChainStages deep,
+// named barriers 1..2*kChainStages), warp 0 runs nothing but the SHA-256 rounds and
+// patches the previous digest into each digest's first block.  The two warps sit on
+// different sub-partitions, so the compression runs at its bare rate.
 template <int DT>
-__global__ void exact_chain_kernel(const void* __restrict__ in, const int64_t* __restrict__ row_off,
-                                   int n_roll, int H, int k, const int64_t* __restrict__ dig_off,
-                                   uint8_t* __restrict__ digests_out) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n_roll) return;
-  const int64_t T = row_off[r + 1] - row_off[r];
-  const int64_t nd = T > 0 ? (T + k - 1) / k : 1;
-  uint32_t prev[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-  uint32_t* out = reinterpret_cast<uint32_t*>(digests_out + 32 * dig_off[r]);
-  for (int64_t j = 0; j < nd; ++j) {
-    const int64_t rows = T > 0 ? min((int64_t)k, T - j * k) : 0;
-    const int64_t base = (row_off[r] + j * k) * (int64_t)H;
-    const int64_t n_el = rows * (int64_t)H;
-    const int64_t n_blocks = (8 + 2 * n_el + 3 + 15) / 16;  // data words + 0x80 word + 64-bit length
-    const uint64_t bits = (uint64_t)(32 + 8 * n_el) * 8u;
-    uint32_t st[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
-                      0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
-    uint64_t ra[8], rb[8];
-    uint32_t w[16], wn[16];
-    fetch_block<DT>(in, base, n_el, 0, ra);
-    assemble_block<DT>(ra, 0, n_el, n_blocks, bits, prev, w);
-    fetch_block<DT>(in, base, n_el, 1, ra);
-    for (int64_t b = 0; b < n_blocks; ++b) {
-      if (8 * (b + kShaPrefetch) - 4 < n_el)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(elem_addr<DT>(in, base + 8 * (b + kShaPrefetch) - 4)));
-      fetch_block<DT>(in, base, n_el, b + 2, rb);
-      assemble_block<DT>(ra, b + 1, n_el, n_blocks, bits, prev, wn);
-      sha256_block(st, w);
+__global__ void __launch_bounds__(64) exact_chain_kernel(const void* __restrict__ in,
+                                                         const int64_t* __restrict__ row_off, int n_roll, int H,
+                                                         int k, const int64_t* __restrict__ dig_off,
+                                                         uint8_t* __restrict__ digests_out) {
+  __shared__ uint32_t ring[kChainStages][16][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.x * 32 + lane;
+  ChainCursor cur;
+  cur.init(r < n_roll ? row_off[r + 1] - row_off[r] : 0, r < n_roll ? row_off[r] : 0, H, k);
+  const int64_t total = r < n_roll ? cur.total_blocks() : 0;
+  int64_t iters = total;  // both warps run the same number of ring steps
 #pragma unroll
-      for (int q = 0; q < 16; ++q) w[q] = wn[q];
+  for (int o = 16; o > 0; o >>= 1) iters = max(iters, (int64_t)__shfl_xor_sync(0xFFFFFFFFu, (long long)iters, o));
+
+  if (warp == 1) {  // ------------------------------------------------ producer
+    const uint32_t zero[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    for (int64_t i = 0; i < iters; ++i) {
+      const int s = (int)(i % kChainStages);
+      if (i >= kChainStages) named_bar_sync(1 + kChainStages + s);  // the consumer has read stage s
+      uint32_t w[16];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) ra[q] = rb[q];
+      for (int q = 0; q < 16; ++q) w[q] = 0u;
+      if (i < total) {
+        if (8 * (cur.b + kShaPrefetch) - 4 < cur.n_el)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(elem_addr<DT>(in, cur.base + 8 * (cur.b + kShaPrefetch) - 4)));
+        uint64_t raw[8];
+        fetch_block<DT>(in, cur.base, cur.n_el, cur.b, raw);
+        assemble_block<DT>(raw, cur.b, cur.n_el, cur.n_blocks, cur.bits(), zero, w);
+        cur.advance();
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) ring[s][q][lane] = w[q];
+      named_bar_arrive(1 + s);  // stage s is full
     }
+    for (int64_t i = max(iters, (int64_t)kChainStages); i < iters + kChainStages; ++i)
+      named_bar_sync(1 + kChainStages + (int)(i % kChainStages));  // match the consumer's last arrivals
+    return;
+  }
+  // ------------------------------------------------------------------ consumer
+  uint32_t prev[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+  uint32_t st[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
+                    0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
+  uint32_t* out = reinterpret_cast<uint32_t*>(digests_out + 32 * (r < n_roll ? dig_off[r] : 0));
+  for (int64_t i = 0; i < iters; ++i) {
+    const int s = (int)(i % kChainStages);
+    named_bar_sync(1 + s);  // stage s is full
+    uint32_t w[16];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      out[8 * j + q] = __byte_perm(st[q], 0u, 0x0123);  // big-endian digest bytes
-      prev[q] = st[q];
+    for (int q = 0; q < 16; ++q) w[q] = ring[s][q][lane];
+    named_bar_arrive(1 + kChainStages + s);  // stage s may be refilled
+    if (i < total) {
+      if (cur.b == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w[q] = prev[q];
+      }
+      sha256_block(st, w);
+      if (cur.b == cur.n_blocks - 1) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          out[8 * cur.j + q] = __byte_perm(st[q], 0u, 0x0123);  // big-endian digest bytes
+          prev[q] = st[q];
+        }
+        st[0] = 0x6a09e667u; st[1] = 0xbb67ae85u; st[2] = 0x3c6ef372u; st[3] = 0xa54ff53au;
+        st[4] = 0x510e527fu; st[5] = 0x9b05688cu; st[6] = 0x1f83d9abu; st[7] = 0x5be0cd19u;
+      }
+      cur.advance();
     }
   }
 }
@@ -1736,7 +1807,7 @@ int tl_exact_chains(const void* hidden, int32_t dtype, const int64_t* row_off, i
   if (n_roll < 0 || H < 0 || k < 1 || dtype < 0 || dtype > 3) return TL_EINVAL;  // H = 0: empty rows
   if (n_roll == 0) return TL_OK;
   if (!hidden || !row_off || !digest_off || !digests_out) return TL_EINVAL;
-  const dim3 grid((n_roll + 31) / 32), block(32);
+  const dim3 grid((n_roll + 31) / 32), block(64);  // 32 rollouts per CTA: a producer and a SHA warp
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (dtype) {
     case 0: exact_chain_kernel<0><<<grid, block, 0, st>>>(hidden, row_off, n_roll, H, k, digest_off, digests_out); break;

@@ -103,10 +103,9 @@ def _staging(dev, elems: int):
 def build_commitments_device(hidden, row_offsets, k: int = 32) -> list[list[bytes]]:
     """Exact-mode commitments with the whole SHA-256 chains on the GPU
     (``tl_exact_chains``, one thread per rollout).  Byte-identical to
-    ``build_commitments`` per rollout.  Each chain is latency-bound (~28 MB/s per
-    thread), so the kernel time is flat in the rollout count: it matches host SHA-NI
-    on all cores at ~1024 rollouts and wins above (``DEVICE_SHA_MIN_ROLLOUTS``,
-    DESIGN §5.6)."""
+    ``build_commitments`` per rollout.  Each chain is latency-bound (~38 MB/s per
+    rollout), so the kernel time is flat in the rollout count: it passes host SHA-NI
+    on all cores at ~700 rollouts (``DEVICE_SHA_MIN_ROLLOUTS``)."""
     if k < 1:
         raise ValueError("interval must be >= 1")
     if not torch.cuda.is_available():
@@ -144,9 +143,9 @@ def build_commitments_device(hidden, row_offsets, k: int = 32) -> list[list[byte
 
 
 # Rollouts from which the GPU chains beat host SHA-NI on all cores
-# (tools/bench_exact.py --device-sweep, H=5120, 2048 tokens: 512 -> 0.35 M vs ~0.63 M
-# tokens/s, 1024 -> 0.68 M vs 0.63 M, 2048 -> 1.34 M vs 0.64 M, 4096 -> 2.70 M vs 0.64 M).
-DEVICE_SHA_MIN_ROLLOUTS = 1024
+# (tools/bench_exact.py --device-sweep, H=5120, 2048 tokens: 512 -> 0.47 M vs 0.62 M
+# tokens/s, 1024 -> 0.93 M vs 0.62 M, 4096 -> 3.46 M vs 0.64 M).
+DEVICE_SHA_MIN_ROLLOUTS = 768
 
 
 def build_commitments_batch(hidden, row_offsets, k: int = 32, threads: int | None = None,
