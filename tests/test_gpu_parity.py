@@ -552,3 +552,36 @@ def test_partitioned_pipeline_short_runs(n):
         vb = eng.verify(dv[k], offs, eng.prove(dp[k], offs))
         assert outs[k].cpu().tolist() == vb.rollout_accept.cpu().tolist(), k
     pipe.close()
+
+
+def test_cross_process_determinism():
+    """Proof bytes, per-chunk statistics and verdicts are a pure function of the input:
+    a fresh process (fresh speculation state, other grid timing) reproduces them bit for
+    bit (the reference's cross-process check, tests/test_policy.py:124-139)."""
+    import subprocess
+    import sys
+    code = r'''
+import hashlib, numpy as np, torch
+from paper_2505_07291_b200 import api
+from paper_2505_07291_b200.synth import synth_device
+offs = np.array([0, 300, 300, 1024, 2048], dtype=np.int64)
+eng = api.engine()
+h = synth_device(2048, 5120, seed=4, dist="massive")
+v = synth_device(2048, 5120, seed=4, dist="massive", jitter_thr=3277, jitter_seed=9)
+pb = eng.prove(h, offs)
+vb = eng.verify(v, offs, pb)
+torch.cuda.synchronize()
+d = hashlib.sha256()
+for t in (pb.proofs, vb.stats, vb.chunk_accept, vb.rollout_accept):
+    d.update(t.cpu().numpy().tobytes())
+print(d.hexdigest())
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = [subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+            for _ in range(2)]
+    for r in runs:
+        assert r.returncode == 0, r.stderr[-2000:]
+    digests = [r.stdout.strip().splitlines()[-1] for r in runs]
+    local = {}
+    exec(code.replace("print(d.hexdigest())", "local['d'] = d.hexdigest()"), {"local": local})
+    assert digests[0] == digests[1] == local["d"]
