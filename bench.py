@@ -444,7 +444,9 @@ def run_b200(args, cfg, rank, world, local_rank):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": world * rows / (float(te.item()) / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "rollouts_per_gpu": Re,
-               "note": "public API (ToplocEngine.prove/verify) from pinned host tensors; proofs and verdicts read back"}
+               "h2d_gbs_per_gpu": h2d / (float(te.item()) / 1e3) / 1e9,
+               "note": "public API (ToplocEngine.prove/verify) from pinned host tensors; proofs and verdicts read "
+                       "back; bound by the host link (h2d_gbs_per_gpu against ~55 GB/s for PCIe 5 x16)"}
 
     peak, peak_src = measured_peak()
     sel_bytes = n_rows * select_bytes_per_token(H)
