@@ -474,10 +474,10 @@ def run_b200(args, cfg, rank, world, local_rank):
                "sample": f"{workers} parallel {args.cpu_tokens}-token slices x H={H} "
                          f"(oracle/toploc_oracle.py prove+verify, one process per core), wall {wall:.1f}s"}
         # the reference's own (exact-mode) path on the same cores, for scale
-        etps, ewall, eok = cpu_sample(1024, H, workers, steps=1, warmup=0, worker=_cpu_exact_worker)
+        etps, ewall, eok = cpu_sample(4096, H, workers, steps=1, warmup=0, worker=_cpu_exact_worker)
         cpu["reference_exact_mode"] = {
             "value": etps, "unit": "tokens/s", "cores": workers, "per_core": etps / workers, "digests_match": eok,
-            "sample": f"{workers} parallel 1024-token slices x H={H}: build_commitments + recompute-and-compare "
+            "sample": f"{workers} parallel 4096-token slices x H={H}: build_commitments + recompute-and-compare "
                       f"(oracle/exact_oracle.py, the reference's rollout.py:51-68), wall {ewall:.1f}s"}
 
     if rank == 0:
