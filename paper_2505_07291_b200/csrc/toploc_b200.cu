@@ -856,6 +856,29 @@ __device__ __forceinline__ void commit_chunk(const uint32_t (&raw)[4], const uin
   __syncwarp();
 }
 
+// ---- TMA bulk copy global -> shared with an mbarrier (the commitment's table staging)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred done;\n WAIT_%=: mbarrier.try_wait.parity.shared.b64 done, [%0], %1;\n"
+      " @!done bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
 // tl_commit: one warp per chunk over (idx, bits) in global memory.  WARPS x 32
 // threads, one CTA per SM, the first prime's inverse table staged in shared memory
 // (HALF = 64 KiB half table and <= 64 registers, so the CTA fits beside 16 one-warp
@@ -871,12 +894,20 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
   uint32_t* xs_all = reinterpret_cast<uint32_t*>(smem_raw + kTabEntries * 2);  // [warps][128]
   uint32_t* cs_all = xs_all + WARPS * 128;                                     // [warps][128]
   uint32_t* hs_all = cs_all + WARPS * 128;                                     // [warps][kHashSlots]
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(inv_tables);
-    uint4* dst = reinterpret_cast<uint4*>(inv0);
-    for (int i = threadIdx.x; i < kTabEntries * 2 / 16; i += WARPS * 32) dst[i] = src[i];
-  }
+  // stage the first prime's inverse table with TMA bulk copies: the whole table is in
+  // flight at once (a load loop over few warps would pay one L2 round trip per step,
+  // ~16 us for a 4-warp CTA -- the small-batch commitment's largest cost)
+  __shared__ __align__(8) uint64_t tab_bar;
+  if (threadIdx.x == 0) mbar_init(&tab_bar, 1);
   __syncthreads();
+  if (threadIdx.x == 0) {
+    constexpr uint32_t kBytes = kTabEntries * 2, kPiece = 32768;
+    mbar_expect_tx(&tab_bar, kBytes);
+#pragma unroll
+    for (uint32_t off = 0; off < kBytes; off += kPiece)
+      bulk_copy_g2s(smem_raw + off, reinterpret_cast<const uint8_t*>(inv_tables) + off, kPiece, &tab_bar);
+  }
+  mbar_wait_parity(&tab_bar, 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* xs = xs_all + warp * 128;
   uint32_t* cs = cs_all + warp * 128;
