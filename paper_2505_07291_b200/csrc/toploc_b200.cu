@@ -698,11 +698,11 @@ __device__ __forceinline__ uint32_t inv_of(const uint16_t* tab, uint32_t d, cons
 // Newton divided differences, levels jl in [j0, j1) with j1 <= 32 (R0 + 1): the
 // register blocks r < R0 are complete (i < jl) and skipped at compile time; in
 // block R0 lanes with i < jl keep their value.  c[i] <- (c[i] - c[i-1]) / (x[i] - x[i-jl]).
-template <int MODE, int R0>
+template <int MODE, int R0, int UNR>
 __device__ __forceinline__ void ndd_levels(int j0, int j1, const uint32_t (&x)[4], uint32_t (&c)[4],
                                            const uint32_t* xs, const ModP& m, const uint16_t* tab, int lane) {
   const int src = (lane + 31) & 31;
-#pragma unroll kNddUnroll
+#pragma unroll UNR
   for (int jl = j0; jl < j1; ++jl) {
     uint32_t t[4];
 #pragma unroll
@@ -722,11 +722,11 @@ __device__ __forceinline__ void ndd_levels(int j0, int j1, const uint32_t (&x)[4
 // The polynomial has degree kk-1-i <= 32 (RM + 1) - 1, so blocks r > RM stay zero.
 // nxs[i] = p - x_i.  Coefficient k takes prev_{k-1} + (p - x_i) a_k (< p^2 < 2^32); the
 // constant term's "previous" is c_i itself, which folds the + c_i into the same reduction.
-template <int RM>
+template <int RM, int UNR>
 __device__ __forceinline__ void conv_steps(int i_hi, int i_lo, uint32_t (&poly)[4], const uint32_t* nxs,
                                            const uint32_t* cs, const ModP& m, int lane) {
   const int src = (lane + 31) & 31;
-#pragma unroll kConvUnroll
+#pragma unroll UNR
   for (int i = i_hi; i >= i_lo; --i) {
     const uint32_t nxi = nxs[i], ci = cs[i];
     uint32_t t[4];
@@ -742,14 +742,14 @@ __device__ __forceinline__ void conv_steps(int i_hi, int i_lo, uint32_t (&poly)[
 
 // Interpolate the warp's kk points (x_i, y_i), i = lane + 32 r, over GF(p):
 // Newton divided differences, then Newton -> monomial.
-template <int MODE>
+template <int MODE, int NU, int CU>
 __device__ __forceinline__ void interpolate_warp(const uint32_t (&x)[4], uint32_t (&c)[4], uint32_t (&poly)[4],
                                                  uint32_t* xs, uint32_t* cs, int kk, const ModP& m,
                                                  const uint16_t* tab, int lane) {
-  ndd_levels<MODE, 0>(1, min(kk, 32), x, c, xs, m, tab, lane);
-  ndd_levels<MODE, 1>(32, min(kk, 64), x, c, xs, m, tab, lane);
-  ndd_levels<MODE, 2>(64, min(kk, 96), x, c, xs, m, tab, lane);
-  ndd_levels<MODE, 3>(96, kk, x, c, xs, m, tab, lane);
+  ndd_levels<MODE, 0, NU>(1, min(kk, 32), x, c, xs, m, tab, lane);
+  ndd_levels<MODE, 1, NU>(32, min(kk, 64), x, c, xs, m, tab, lane);
+  ndd_levels<MODE, 2, NU>(64, min(kk, 96), x, c, xs, m, tab, lane);
+  ndd_levels<MODE, 3, NU>(96, kk, x, c, xs, m, tab, lane);
   __syncwarp();  // every lane is done reading xs
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -761,10 +761,10 @@ __device__ __forceinline__ void interpolate_warp(const uint32_t (&x)[4], uint32_
   for (int r = 0; r < 4; ++r) poly[r] = 0u;
   if (lane == 0) poly[0] = cs[kk - 1];
   // step i yields degree kk-1-i: blocks r <= (kk-1-i) >> 5 are live
-  conv_steps<0>(kk - 2, max(kk - 32, 0), poly, xs, cs, m, lane);
-  conv_steps<1>(kk - 33, max(kk - 64, 0), poly, xs, cs, m, lane);
-  conv_steps<2>(kk - 65, max(kk - 96, 0), poly, xs, cs, m, lane);
-  conv_steps<3>(kk - 97, 0, poly, xs, cs, m, lane);
+  conv_steps<0, CU>(kk - 2, max(kk - 32, 0), poly, xs, cs, m, lane);
+  conv_steps<1, CU>(kk - 33, max(kk - 64, 0), poly, xs, cs, m, lane);
+  conv_steps<2, CU>(kk - 65, max(kk - 96, 0), poly, xs, cs, m, lane);
+  conv_steps<3, CU>(kk - 97, 0, poly, xs, cs, m, lane);
 }
 
 // One warp commits one chunk: modulus search, GF(p) interpolation and the 258-byte
@@ -798,7 +798,7 @@ __device__ __forceinline__ bool residues_distinct(const uint32_t (&res)[4], int 
   return !any_dup;
 }
 
-template <int MODE0>
+template <int MODE0, int NU = kNddUnroll, int CU = kConvUnroll>
 __device__ __forceinline__ void commit_chunk(const uint32_t (&raw)[4], const uint32_t (&yb)[4], int kk, int K,
                                              const uint16_t* tab0, const uint16_t* __restrict__ inv_tables,
                                              uint32_t* xs, uint32_t* cs, uint32_t* hs, uint8_t* __restrict__ pr,
@@ -838,9 +838,9 @@ __device__ __forceinline__ void commit_chunk(const uint32_t (&raw)[4], const uin
     xs[i] = x[r];
   }
   __syncwarp();
-  if (pi == 0) interpolate_warp<MODE0>(x, c, poly, xs, cs, kk, m, tab0, lane);
-  else if (pi < kInvTables) interpolate_warp<kInvGlobal>(x, c, poly, xs, cs, kk, m, inv_tables + (size_t)pi * 65536u, lane);
-  else interpolate_warp<kInvFermat>(x, c, poly, xs, cs, kk, m, nullptr, lane);
+  if (pi == 0) interpolate_warp<MODE0, NU, CU>(x, c, poly, xs, cs, kk, m, tab0, lane);
+  else if (pi < kInvTables) interpolate_warp<kInvGlobal, NU, CU>(x, c, poly, xs, cs, kk, m, inv_tables + (size_t)pi * 65536u, lane);
+  else interpolate_warp<kInvFermat, NU, CU>(x, c, poly, xs, cs, kk, m, nullptr, lane);
 
   // ---- serialise: p, c_0..c_{K-1}, u16 big-endian
   uint16_t* pw = reinterpret_cast<uint16_t*>(pr);
@@ -929,8 +929,10 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
       yb[r] = b;
       kk += __popc(__ballot_sync(0xFFFFFFFFu, iv >= 0));
     }
-    commit_chunk<HALF ? kInvSmemHalf : kInvSmem>(raw, yb, kk, K, inv0, inv_tables, xs, cs, hs, proofs + j * PB,
-                                                 lane);
+    // a small-batch CTA (one chunk per sub-partition) is latency-bound: unroll deeper so the
+    // inverse lookups of later levels are issued ahead of the divided-difference chain
+    commit_chunk<HALF ? kInvSmemHalf : kInvSmem, WARPS <= 4 ? 8 : kNddUnroll, WARPS <= 4 ? 4 : kConvUnroll>(
+        raw, yb, kk, K, inv0, inv_tables, xs, cs, hs, proofs + j * PB, lane);
     j = nw + (int64_t)__shfl_sync(0xFFFFFFFFu, claim, 0);
   }
 }
