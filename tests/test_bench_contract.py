@@ -30,6 +30,8 @@ def test_reference_arm_prints_one_contract_line():
     assert d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["config"]["workload"].startswith("configs[0]")
+    ex = d["cpu_baseline"]["reference_exact_mode"]  # the reference's own path, for scale
+    assert ex["value"] > 0 and ex["digests_match"] is True
 
 
 def test_warmup_below_three_is_rejected():
