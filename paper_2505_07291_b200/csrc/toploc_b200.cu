@@ -55,6 +55,11 @@ constexpr unsigned kIdxMask = 0xFFFFFFu;      // flat index field (24 bits)
 constexpr int kInvTables = 8;                 // precomputed inverse tables (first 8 primes)
 constexpr int kHashBits = 8;                  // injectivity check: 256-slot set per commit warp
 constexpr int kHashSlots = 1 << kHashBits;
+constexpr int kSplitMax = 8;            // small batches: up to 8 warps share one chunk
+constexpr int kSplitMaxLists = 4096;    // partial top-k lists in the workspace
+constexpr int kSplitMaxChunks = 2048;   // chunk arrival counters in the workspace
+constexpr int kSplitMinPart = 32768;    // elements per part, at least: a part pays a whole chunk's
+                                        // final sort, so it must stream long enough to amortise it
 constexpr int kSpecSlots = 8192;              // speculation slots in the workspace (16 B each)
 #ifndef TL_COMMIT_WARPS
 #define TL_COMMIT_WARPS 32
@@ -284,6 +289,9 @@ struct SelArgs {
   unsigned long long* next;  // workspace: chunks handed out beyond the first round (reset by chunk_prefix_kernel)
   int n_roll, H, C, K;
   int64_t n_chunks;  // caller's n_chunks (clamped to prefix[n_roll] in the kernels)
+  int split = 1;                            // warps per chunk (small batches, sel_plan)
+  unsigned long long* part = nullptr;       // workspace: [n_chunks][split][K] partial top-k keys
+  unsigned* part_cnt = nullptr;             // workspace: per-chunk arrivals (zeroed by chunk_prefix_kernel)
 };
 // Chunk scheduling: the first round is static (chunk = global warp id), later chunks
 // are claimed from a workspace counter, so warps that stream faster (SMs with fewer
@@ -562,13 +570,99 @@ __device__ int select_chunk(const ChunkGeo& cg, int kk, WarpSlot& slot, Spec& sp
   return cnt;
 }
 
+// ---- small batches: S warps share a chunk
+// Part s of a chunk is the element range [lo, hi) (8-element aligned relative to the
+// chunk).  The chunk's top-kk is contained in the union of its parts' top-kk, and a
+// part's keys become chunk keys by re-basing the index (key - (lo << 16): the index is
+// stored as kIdxMask - idx).  The last part to finish merges the lists.
+__device__ __forceinline__ ChunkGeo sub_geo(const ChunkGeo& g, int lo, int hi) {
+  ChunkGeo s;
+  s.base = g.base + lo;
+  s.n = hi - lo;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(s.base);
+  s.a0 = min(s.n, (int)(((16u - (unsigned)(addr & 15u)) & 15u) >> 1));
+  s.nvec = (s.n - s.a0) >> 3;
+  s.nst = (s.nvec + kWTileVec - 1) / kWTileVec;
+  return s;
+}
+
+// Sort a bitonic sequence of 128 keys (a[r] at position 32 r + lane) descending.
+__device__ __forceinline__ void bitonic_merge_desc128(unsigned long long (&a)[4], int lane) {
+#pragma unroll
+  for (int rj = 2; rj >= 1; rj >>= 1) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if ((r & rj) == 0) {
+        const unsigned long long x = a[r], y = a[r | rj];
+        a[r] = x > y ? x : y;
+        a[r | rj] = x > y ? y : x;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 16; j >= 1; j >>= 1) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const unsigned long long y = __shfl_xor_sync(0xFFFFFFFFu, a[r], j);
+      a[r] = (lane & j) ? (a[r] < y ? a[r] : y) : (a[r] > y ? a[r] : y);
+    }
+  }
+}
+
+// Part s of chunk j: select its top-k and publish it; if this is the chunk's last part
+// to finish, merge every part into slot.wbuf[0..kk) and return true.
+__device__ __forceinline__ bool select_split(const SelArgs& a, const ChunkGeo& g, int kk, int64_t j, int s,
+                                          WarpSlot& slot, Spec& sp, int lane PROF_ARG) {
+  const int S = a.split, K = a.K;
+  const int lo = s == 0 ? 0 : (int)(((int64_t)g.n * s / S) & ~7ll);
+  const int hi = s == S - 1 ? g.n : (int)(((int64_t)g.n * (s + 1) / S) & ~7ll);
+  const int kks = min(K, hi - lo);
+  if (kks > 0) select_chunk(sub_geo(g, lo, hi), kks, slot, sp, lane PROF_PASS);
+  unsigned long long* mine = a.part + ((size_t)j * S + s) * K;
+  for (int i = lane; i < K; i += 32) mine[i] = i < kks ? slot.wbuf[i] - ((unsigned long long)lo << 16) : 0ull;
+  __threadfence();
+  __syncwarp();
+  unsigned arrived = 0;
+  if (lane == 0) arrived = atomicAdd(a.part_cnt + j, 1u);
+  arrived = __shfl_sync(0xFFFFFFFFu, arrived, 0);
+  if (arrived != (unsigned)(S - 1)) return false;
+  __threadfence();
+  // top-K of the union: acc <- bitonic merge of (acc, list q reversed), one list at a time
+  const unsigned long long* parts = a.part + (size_t)j * S * K;
+  unsigned long long acc[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int p = 32 * r + lane;
+    acc[r] = p < K ? __ldcg(parts + p) : 0ull;
+  }
+  for (int q = 1; q < S; ++q) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int p = 127 - (32 * r + lane);
+      const unsigned long long b = p < K ? __ldcg(parts + (size_t)q * K + p) : 0ull;
+      acc[r] = acc[r] > b ? acc[r] : b;
+    }
+    bitonic_merge_desc128(acc, lane);
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int p = 32 * r + lane;
+    if (p < kk) slot.wbuf[p] = acc[r];
+  }
+  __syncwarp();
+  return true;
+}
+
 // ----------------------------------------------------------------------------- kernels
 __global__ void chunk_prefix_kernel(const int64_t* __restrict__ row_off, int n_roll, int C,
-                                    int64_t* __restrict__ prefix, unsigned long long* __restrict__ next_chunk) {
+                                    int64_t* __restrict__ prefix, unsigned long long* __restrict__ next_chunk,
+                                    unsigned* __restrict__ part_cnt) {
   __shared__ int64_t warp_tot[32];
   __shared__ int64_t carry;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) { carry = 0; prefix[0] = 0; *next_chunk = 0; }
+  if (part_cnt)
+    for (int i = tid; i < kSplitMaxChunks; i += blockDim.x) part_cnt[i] = 0u;
   __syncthreads();
   for (int base = 0; base < n_roll; base += blockDim.x) {
     const int r = base + tid;
@@ -601,6 +695,7 @@ __global__ void chunk_prefix_kernel(const int64_t* __restrict__ row_off, int n_r
   }
 }
 
+template <bool SPLIT>
 __global__ void __launch_bounds__(kSelBlockThreads, kSelMinBlocks)
 prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restrict__ bits_out) {
   extern __shared__ __align__(128) uint8_t sel_smem[];
@@ -614,12 +709,17 @@ prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restri
   const int64_t gw = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5);
   Spec sp = spec_load(a.spec, gw);
   PROF_DECL;
-  for (int64_t j = gw; j < n_chunks;) {
-    const unsigned long long claim = claim_chunk(a, lane);
+  const int S = SPLIT ? a.split : 1;
+  for (int64_t j = SPLIT ? gw / S : gw; j < n_chunks;) {
+    const unsigned long long claim = SPLIT ? 0ull : claim_chunk(a, lane);
     const ChunkGeo g = chunk_geo(a, j);
     const int kk = min(K, g.n);
     PROF_MARK(0);
-    select_chunk(g, kk, slot, sp, lane PROF_PASS);
+    if (SPLIT) {
+      if (!select_split(a, g, kk, j, (int)(gw % S), slot, sp, lane PROF_PASS)) break;  // another part merges
+    } else {
+      select_chunk(g, kk, slot, sp, lane PROF_PASS);
+    }
     for (int i = lane; i < K; i += 32) {
       if (i < kk) {
         const unsigned long long v = slot.wbuf[i];
@@ -632,6 +732,7 @@ prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restri
     }
     __syncwarp();
     PROF_MARK(4);
+    if (SPLIT) break;  // one part per warp
     j = nw + (int64_t)__shfl_sync(0xFFFFFFFFu, claim, 0);
   }
   spec_store(a.spec, gw, sp, lane);
@@ -942,6 +1043,7 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
 // the claimed polynomial at the kk indices (Horner, four points per lane),
 // compares exponent and mantissa bits with the observed values mod p, and writes
 // the chunk statistics and verdict.
+template <bool SPLIT>
 __global__ void __launch_bounds__(kSelBlockThreads, kSelMinBlocks)
 verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
               tl_chunk_stats* __restrict__ stats_out, uint8_t* __restrict__ accept_out) {
@@ -958,8 +1060,9 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
   const int64_t gw = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5);
   Spec sp = spec_load(a.spec, gw);
   PROF_DECL;
-  for (int64_t j = gw; j < n_chunks;) {
-    const unsigned long long claim = claim_chunk(a, lane);
+  const int S = SPLIT ? a.split : 1;
+  for (int64_t j = SPLIT ? gw / S : gw; j < n_chunks;) {
+    const unsigned long long claim = SPLIT ? 0ull : claim_chunk(a, lane);
     const ChunkGeo g = chunk_geo(a, j);
     const int kk = min(K, g.n);
     // issue this chunk's proof loads (u16 t = p or c_{t-1}) before streaming, so
@@ -972,7 +1075,11 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
       pword[q] = t <= K ? (uint32_t)__ldg(pw + t) : 0u;
     }
     PROF_MARK(0);
-    select_chunk(g, kk, slot, sp, lane PROF_PASS);
+    if (SPLIT) {
+      if (!select_split(a, g, kk, j, (int)(gw % S), slot, sp, lane PROF_PASS)) break;  // another part merges
+    } else {
+      select_chunk(g, kk, slot, sp, lane PROF_PASS);
+    }
 
     // claimed coefficients (big-endian u16) -> slot.coef, zero-padded to TL_MAX_K
     unsigned p = 0;
@@ -1076,6 +1183,7 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
     }
     __syncwarp();
     PROF_MARK(4);
+    if (SPLIT) break;  // one part per warp
     j = nw + (int64_t)__shfl_sync(0xFFFFFFFFu, claim, 0);
   }
   spec_store(a.spec, gw, sp, lane);
@@ -1457,7 +1565,7 @@ __global__ void synth_kernel(uint16_t* __restrict__ out, int64_t row0, int64_t n
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t spec, next, prefix, tables, idx, bits, accept, total;
+  size_t spec, next, prefix, tables, idx, bits, accept, part, part_cnt, total;
 };
 WsLayout ws_layout(int32_t n_roll, int64_t n_chunks, int32_t K) {
   WsLayout L;
@@ -1469,6 +1577,8 @@ WsLayout ws_layout(int32_t n_roll, int64_t n_chunks, int32_t K) {
   L.idx = o; o = align_up(o + (size_t)n_chunks * K * 4, 256);
   L.bits = o; o = align_up(o + (size_t)n_chunks * K * 2, 256);
   L.accept = o; o = align_up(o + (size_t)n_chunks, 256);
+  L.part = o; o = align_up(o + (size_t)kSplitMaxLists * TL_MAX_K * 8, 256);
+  L.part_cnt = o; o = align_up(o + (size_t)kSplitMaxChunks * 4, 256);
   L.total = o;
   return L;
 }
@@ -1565,6 +1675,26 @@ int sel_grid(int64_t n_chunks, const void* kernel, cudaStream_t st, int ctas_per
   return (int)((warps + kSelWarps - 1) / kSelWarps);
 }
 
+// Grid and warps-per-chunk of a streaming launch.  A batch too small to give every warp
+// slot of the grid a chunk splits each chunk over up to kSplitMax warps (each part at
+// least kSplitMinPart elements): small batches are latency-bound per warp, and more
+// warps per chunk fill the GPU.
+struct SelPlan { int grid, split; };
+SelPlan sel_plan(int64_t n_chunks, int64_t chunk_elems, const void* kernel, cudaStream_t st, int ctas_per_sm) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSelBlockThreads, kSelSmem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  if (ctas_per_sm > 0 && ctas_per_sm < per_sm) per_sm = ctas_per_sm;
+  const int64_t wmax = (int64_t)stream_sms(st) * per_sm * kSelWarps;
+  int64_t split = n_chunks > 0 ? wmax / n_chunks : 1;
+  split = min(split, (int64_t)kSplitMax);
+  split = min(split, chunk_elems / kSplitMinPart);
+  if (n_chunks > kSplitMaxChunks || split * n_chunks > kSplitMaxLists) split = 1;
+  if (split >= 2) return {(int)((n_chunks * split + kSelWarps - 1) / kSelWarps), (int)split};
+  return {sel_grid(n_chunks, kernel, st, ctas_per_sm), 1};
+}
+
 int launch_status() { return cudaGetLastError() == cudaSuccess ? TL_OK : TL_ECUDA; }
 
 template <int WARPS, bool HALF>
@@ -1647,16 +1777,24 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   int64_t* prefix = reinterpret_cast<int64_t*>(ws + L.prefix);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned* part_cnt = reinterpret_cast<unsigned*>(ws + L.part_cnt);
   chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix,
-                                          reinterpret_cast<unsigned long long*>(ws + L.next));
-  const SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
-                  reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
-  if (cudaFuncSetAttribute(prove_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
-      cudaSuccess)
+                                          reinterpret_cast<unsigned long long*>(ws + L.next), part_cnt);
+  SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
+            reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
+  if (cudaFuncSetAttribute(prove_select_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kSelSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(prove_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kSelSmem) != cudaSuccess)
     return TL_ECUDA;
-  prove_select_kernel<<<sel_grid(n_chunks, (const void*)prove_select_kernel, st, ctas_per_sm), kSelBlockThreads,
-                        kSelSmem, st>>>(
-      a, idx_out, bits_out);
+  const SelPlan sp = sel_plan(n_chunks, (int64_t)C * H, (const void*)prove_select_kernel<false>, st, ctas_per_sm);
+  a.split = sp.split;
+  a.part = reinterpret_cast<unsigned long long*>(ws + L.part);
+  a.part_cnt = part_cnt;
+  if (sp.split > 1)
+    prove_select_kernel<true><<<sp.grid, kSelBlockThreads, kSelSmem, st>>>(a, idx_out, bits_out);
+  else
+    prove_select_kernel<false><<<sp.grid, kSelBlockThreads, kSelSmem, st>>>(a, idx_out, bits_out);
   return launch_status();
 }
 
@@ -1739,17 +1877,27 @@ int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   uint8_t* accept = chunk_accept_out ? chunk_accept_out : ws + L.accept;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
+  unsigned* part_cnt = reinterpret_cast<unsigned*>(ws + L.part_cnt);
   chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix,
-                                          reinterpret_cast<unsigned long long*>(ws + L.next));
+                                          reinterpret_cast<unsigned long long*>(ws + L.next), part_cnt);
   if (n_chunks > 0) {
-    const SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
-                  reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
-    if (cudaFuncSetAttribute(verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
-        cudaSuccess)
+    SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
+              reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
+    if (cudaFuncSetAttribute(verify_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(verify_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
+            cudaSuccess)
       return TL_ECUDA;
-    verify_kernel<<<sel_grid(n_chunks, (const void*)verify_kernel, st, ctas_per_sm), kSelBlockThreads, kSelSmem,
-                    st>>>(
-        a, proofs, *thresholds_host, stats_out, accept);
+    const SelPlan sp = sel_plan(n_chunks, (int64_t)C * H, (const void*)verify_kernel<false>, st, ctas_per_sm);
+    a.split = sp.split;
+    a.part = reinterpret_cast<unsigned long long*>(ws + L.part);
+    a.part_cnt = part_cnt;
+    if (sp.split > 1)
+      verify_kernel<true><<<sp.grid, kSelBlockThreads, kSelSmem, st>>>(a, proofs, *thresholds_host, stats_out,
+                                                                        accept);
+    else
+      verify_kernel<false><<<sp.grid, kSelBlockThreads, kSelSmem, st>>>(a, proofs, *thresholds_host, stats_out,
+                                                                         accept);
   }
   if (rollout_accept_out)
     rollout_verdict_kernel<<<(n_roll + 7) / 8, 256, 0, st>>>(accept, prefix, n_roll, rollout_accept_out);
