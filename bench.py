@@ -36,10 +36,10 @@ CHUNK, TOPK = 32, 128
 PROOF_BYTES = 2 + 2 * TOPK
 JITTER_THR = 3277          # 5 % of elements +-1 ulp in the validator's recompute
 # --schedule auto: the partitioned pipeline from this many chunks per GPU, one CUDA graph per
-# step below.  Measured: configuration 1 (64 chunks, H 1024) graph 0.080 ms vs partition
-# 0.115 ms; H 5120 at 256 / 1024 / 4096 / 16384 chunks partition 0.123 / 0.179 / 0.440 /
-# 1.534 ms vs graph 0.174 / 0.224 / 0.554 / 1.884 ms.
-AUTO_PIPELINE_MIN_CHUNKS = 256
+# step below.  Measured (ms per step, graph vs partition): configuration 1 (64 chunks, H 1024)
+# 0.068 vs 0.115; H 5120 at 256 / 1024 chunks 0.113 vs 0.118 / 0.208 vs 0.161; 4096 / 16384
+# chunks 0.554 vs 0.440 / 1.884 vs 1.534.
+AUTO_PIPELINE_MIN_CHUNKS = 512
 LAUNCHES_PER_STEP = 7      # select: prefix+select; commit: inv_table+commit; verify: prefix+verify+verdict
 
 
@@ -541,7 +541,7 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=8192)
     ap.add_argument("--no-spot-check", dest="spot_check", action="store_false")
     ap.add_argument("--schedule", default="auto", choices=["auto", "partition", "pipeline", "serial", "graph"],
-                    help="auto (default): partition from 256 chunks per GPU (AUTO_PIPELINE_MIN_CHUNKS), graph below; "
+                    help="auto (default): partition from 512 chunks per GPU (AUTO_PIPELINE_MIN_CHUNKS), graph below; "
                          "partition: the pipeline on two SM partitions (green contexts), commit on "
                          "--commit-sms SMs, select/verify on the rest; "
                          "pipeline: commit(k) on a side stream, co-resident with verify(k-1) and select(k+1); "
