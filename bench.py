@@ -37,7 +37,7 @@ PROOF_BYTES = 2 + 2 * TOPK
 JITTER_THR = 3277          # 5 % of elements +-1 ulp in the validator's recompute
 # --schedule auto: the partitioned pipeline from this many chunks per GPU, one CUDA graph per
 # step below.  Measured (ms per step, graph vs partition): configuration 1 (64 chunks, H 1024)
-# 0.068 vs 0.115; H 5120 at 256 / 1024 chunks 0.113 vs 0.118 / 0.208 vs 0.161; 4096 / 16384
+# 0.066 vs 0.115; H 5120 at 256 / 1024 chunks 0.113 vs 0.118 / 0.208 vs 0.161; 4096 / 16384
 # chunks 0.554 vs 0.440 / 1.884 vs 1.534.
 AUTO_PIPELINE_MIN_CHUNKS = 512
 LAUNCHES_PER_STEP = 7      # select: prefix+select; commit: inv_table+commit; verify: prefix+verify+verdict

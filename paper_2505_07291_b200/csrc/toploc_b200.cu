@@ -55,10 +55,11 @@ constexpr unsigned kIdxMask = 0xFFFFFFu;      // flat index field (24 bits)
 constexpr int kInvTables = 8;                 // precomputed inverse tables (first 8 primes)
 constexpr int kHashBits = 8;                  // injectivity check: 256-slot set per commit warp
 constexpr int kHashSlots = 1 << kHashBits;
-constexpr int kSplitMax = 8;            // small batches: up to 8 warps share one chunk
+constexpr int kSplitMax = 5;            // small batches: up to 5 warps share one chunk (the last one
+                                        // merges the others' lists: more parts cost more merge steps)
 constexpr int kSplitMaxLists = 4096;    // partial top-k lists in the workspace
 constexpr int kSplitMaxChunks = 2048;   // chunk arrival counters in the workspace
-constexpr int kSplitMinPart = 32768;    // elements per part, at least: a part pays a whole chunk's
+constexpr int kSplitMinPart = 16384;    // elements per part, at least: a part pays a whole chunk's
                                         // final sort, so it must stream long enough to amortise it
 constexpr int kSpecSlots = 8192;              // speculation slots in the workspace (16 B each)
 #ifndef TL_COMMIT_WARPS
