@@ -588,14 +588,15 @@ print(d.hexdigest())
 
 
 @pytest.mark.parametrize("H,C,K,offs", [
-    (2048, 32, 128, [0, 32, 65, 97]),        # 2 parts per chunk, a 1-row chunk
-    (8192, 32, 128, [0, 33, 64]),            # 8 parts per chunk
-    (16, 8192, 128, [0, 8197]),              # 4 parts; the 5-row tail chunk has parts < K and empty parts
+    (2048, 32, 128, [0, 32, 65, 97]),        # 4 parts per chunk, a 1-row chunk
+    (8192, 32, 128, [0, 33, 64]),            # 5 parts per chunk
+    (16, 8192, 128, [0, 8197]),              # 5 parts; the 5-row tail chunk has parts < K and empty parts
     (5120, 32, 5, [0, 40, 41]),              # 5 parts, K = 5
+    (1024, 32, 128, [0, 64, 100]),           # configuration 1's shape: 2 parts
 ])
 def test_split_chunks_match_oracle(H, C, K, offs):
-    """Small batches split each chunk over several warps (csrc select_split: parts of
-    >= 32K elements, the last part merges the partial top-k lists).  Bit-exact against
+    """Small batches split each chunk over several warps (csrc select_split: up to 5 parts
+    of >= 16K elements, the last part merges the partial top-k lists).  Bit-exact against
     the oracle for prove and verify, including parts smaller than K and empty parts."""
     bits = synth_bits(0, offs[-1], H, seed=H + C + K, dist=1)
     _, proofs = check_prove_against_oracle(bits, offs, K=K, C=C)
