@@ -6,7 +6,6 @@ prompt + output[:t]) -- and the validator's teacher-forced ``prefill_rows`` yiel
 same rows.  GPU: proofs built from the capture buffer verify against the validator's
 prefill, and a different model is rejected."""
 
-import numpy as np
 import pytest
 import torch
 
