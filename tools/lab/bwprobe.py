@@ -1,5 +1,5 @@
 """Read-bandwidth ceiling on this B200 (lab): python tools/lab/bwprobe.py"""
-import ctypes, json, os, sys
+import ctypes, json, os
 import torch
 lib = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbwprobe.so"))
 lib.probe.restype = ctypes.c_float
