@@ -466,6 +466,29 @@ def run_b200(args, cfg, rank, world, local_rank):
         except Exception:
             pass
 
+    # the reference's own (exact-mode) algorithm on this GPU, for scale: whole SHA-256
+    # chains over round(h, 6) (tl_exact_chains), checked against the host chains
+    exact = None
+    if args.exact and rank == 0 and world == 1:
+        from paper_2505_07291_b200.exact import build_commitments_batch
+        Rx, Tx = 4096, 256
+        hx = torch.empty((Rx * Tx, H), dtype=torch.bfloat16, device=dev)
+        synth_device(Rx * Tx, H, seed=11, device=dev, out=hx)
+        ox = np.arange(Rx + 1, dtype=np.int64) * Tx
+        build_commitments_batch(hx[:Tx], ox[:2], 32, sha="device")  # warm-up
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        dg = build_commitments_batch(hx, ox, 32, sha="device")
+        tx = time.perf_counter() - t0
+        ok = all(dg[r] == build_commitments_batch(hx[r * Tx:(r + 1) * Tx], ox[:2], 32, sha="host")[0]
+                 for r in (0, Rx - 1))
+        exact = {"value": Rx * Tx / tx, "unit": "tokens/s", "rollouts": Rx, "tokens_per_rollout": Tx,
+                 "digests_match_host": ok,
+                 "note": "the reference's exact-mode commitments (rollout.py:51-68) as whole SHA-256 chains on "
+                         "the GPU, one lane per rollout, wall time including the digest read-back; compare "
+                         "cpu_baseline.reference_exact_mode"}
+        del hx
+
     cpu = None
     if args.cpu_baseline and rank == 0 and world == 1:
         workers = cpu_workers()
@@ -516,6 +539,7 @@ def run_b200(args, cfg, rank, world, local_rank):
                                        "graph: serial step replayed as one CUDA graph" if args.schedule == "graph"
                                        else "serial")},
             "cpu_baseline": cpu,
+            "exact_mode": exact,
             "e2e": e2e,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
             "clocks": clk,
@@ -538,6 +562,8 @@ def main():
     ap.add_argument("--e2e-rollouts", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-exact", dest="exact", action="store_false",
+                    help="skip the exact-mode (reference algorithm) GPU measurement")
     ap.add_argument("--cpu-tokens", type=int, default=8192)
     ap.add_argument("--no-spot-check", dest="spot_check", action="store_false")
     ap.add_argument("--schedule", default="auto", choices=["auto", "partition", "pipeline", "serial", "graph"],
