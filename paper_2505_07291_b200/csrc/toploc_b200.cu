@@ -1448,7 +1448,7 @@ __global__ void __launch_bounds__(64) exact_chain_kernel(const void* __restrict_
                                                          const int64_t* __restrict__ row_off, int n_roll, int H,
                                                          int k, const int64_t* __restrict__ dig_off,
                                                          uint8_t* __restrict__ digests_out) {
-  __shared__ uint32_t ring[kChainStages][16][32];
+  __shared__ uint4 ring[kChainStages][4][32];  // 16 words per lane as 4 x 16 B, lane-interleaved (conflict-free)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.x * 32 + lane;
   ChainCursor cur;
@@ -1475,7 +1475,7 @@ __global__ void __launch_bounds__(64) exact_chain_kernel(const void* __restrict_
         cur.advance();
       }
 #pragma unroll
-      for (int q = 0; q < 16; ++q) ring[s][q][lane] = w[q];
+      for (int q = 0; q < 4; ++q) ring[s][q][lane] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
       named_bar_arrive(1 + s);  // stage s is full
     }
     for (int64_t i = max(iters, (int64_t)kChainStages); i < iters + kChainStages; ++i)
@@ -1492,7 +1492,10 @@ __global__ void __launch_bounds__(64) exact_chain_kernel(const void* __restrict_
     named_bar_sync(1 + s);  // stage s is full
     uint32_t w[16];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) w[q] = ring[s][q][lane];
+    for (int q = 0; q < 4; ++q) {
+      const uint4 v = ring[s][q][lane];
+      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
     named_bar_arrive(1 + kChainStages + s);  // stage s may be refilled
     if (i < total) {
       if (cur.b == 0) {
