@@ -603,3 +603,22 @@ def test_split_chunks_match_oracle(H, C, K, offs):
     jit = synth_bits(0, offs[-1], H, seed=H + C + K, dist=1, jitter_thr=3277, jitter_seed=2)
     check_verify_against_oracle(jit, offs, proofs, K=K, C=C)
     check_verify_against_oracle(bits, offs, proofs, K=K, C=C)
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_fuzz_split_chunks(case):
+    """Seeded random small batches of wide chunks, so the kernels split chunks over
+    several warps (odd H, C and K away from the defaults, ragged rollouts, all value
+    distributions, a jittered validator) -- against the oracle."""
+    rng = np.random.default_rng(5000 + case)
+    H = int(rng.choice([2048, 3001, 4096, 5120, 8192]))
+    C = int(rng.choice([16, 32, 32]))
+    K = int(rng.choice([1, 64, 128, 128]))
+    lens = rng.integers(1, 2 * C + 9, size=int(rng.integers(1, 4)))
+    offs = [0] + np.cumsum(lens).tolist()
+    dist = int(rng.integers(0, 4))
+    bits = synth_bits(0, offs[-1], H, seed=case, dist=dist)
+    _, proofs = check_prove_against_oracle(bits, offs, K=K, C=C)
+    jit = synth_bits(0, offs[-1], H, seed=case, dist=dist, jitter_thr=int(rng.integers(0, 20000)),
+                     jitter_seed=case + 3)
+    check_verify_against_oracle(jit, offs, proofs, K=K, C=C)
