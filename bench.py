@@ -35,11 +35,13 @@ CONFIGS = {
 CHUNK, TOPK = 32, 128
 PROOF_BYTES = 2 + 2 * TOPK
 JITTER_THR = 3277          # 5 % of elements +-1 ulp in the validator's recompute
-# --schedule auto: the partitioned pipeline from this many chunks per GPU, one CUDA graph per
-# step below.  Measured (ms per step, graph vs partition): configuration 1 (64 chunks, H 1024)
-# 0.066 vs 0.115; H 5120 at 256 / 1024 chunks 0.113 vs 0.118 / 0.208 vs 0.161; 4096 / 16384
-# chunks 0.554 vs 0.440 / 1.884 vs 1.534.
-AUTO_PIPELINE_MIN_CHUNKS = 512
+# --schedule auto: the partitioned pipeline from this many chunks per GPU; below it the
+# three-stream pipeline captured as one CUDA graph (small batches: every kernel is
+# latency-bound and the stages of different batches overlap).  Measured ms per step,
+# pipegraph / graph / partition: configuration 1 (64 chunks, H 1024) 0.047 / 0.066 / 0.115;
+# H 5120 at 256 chunks 0.078 / 0.113 / 0.118, 1024 chunks 0.146 / 0.208 / 0.161, 2048 chunks
+# 0.268 / - / 0.257, 4096 chunks 0.431 / 0.554 / 0.432.
+AUTO_PIPELINE_MIN_CHUNKS = 2048
 LAUNCHES_PER_STEP = 7      # select: prefix+select; commit: inv_table+commit; verify: prefix+verify+verdict
 
 
@@ -299,7 +301,7 @@ def run_b200(args, cfg, rank, world, local_rank):
 
     if args.schedule == "auto":
         # small batches are latency-bound: one CUDA graph per step beats the pipelines
-        args.schedule = "partition" if plan.n_chunks >= AUTO_PIPELINE_MIN_CHUNKS else "graph"
+        args.schedule = "partition" if plan.n_chunks >= AUTO_PIPELINE_MIN_CHUNKS else "pipegraph"
     args.pipeline_on = args.schedule in ("pipeline", "partition")
     pipe = None
     if args.schedule == "partition":
@@ -311,6 +313,12 @@ def run_b200(args, cfg, rank, world, local_rank):
     if pipe is None:
         pipe = api.Pipeline(eng, offs, H, ctas_per_sm=args.ctas) if args.pipeline_on else None
     graph = api.StepGraph(plan, prv, val) if args.schedule == "graph" else None
+    pgraph = None
+    if args.schedule == "pipegraph":
+        pgraph_pipe = api.DualStreamPipeline(eng, offs, H)
+        for _ in range(args.warmup):
+            pgraph_pipe.run([prv], [val])
+        pgraph = api.PipelineGraph(pgraph_pipe, [prv] * args.steps, [val] * args.steps)
     if graph is not None:
         for _ in range(args.warmup):
             graph.replay()
@@ -360,6 +368,17 @@ def run_b200(args, cfg, rank, world, local_rank):
         torch.cuda.synchronize(dev)
         sel_ms, com_ms, ver_ms = serial_ms["select"], serial_ms["commit"], serial_ms["verify"]
         accepted = int(plan.rollout_accept.sum().item())
+    elif args.schedule == "pipegraph":
+        t_start.record(stream)
+        outs = pgraph.replay()  # all K batches, pipelined, one graph launch
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+        sel_ms, com_ms, ver_ms = serial_ms["select"], serial_ms["commit"], serial_ms["verify"]
+        accepted = int(outs[-1].sum().item())
+        assert all(int(o.sum().item()) == accepted for o in outs)
+        spot_pipe = bool(torch.equal(pgraph_pipe.plans[(args.steps - 1) % 3].proofs, plan.proofs))
+        if spot is not None:
+            spot["pipeline_proofs_equal_serial"] = spot_pipe
     else:
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
         t_start.record(stream)
@@ -537,6 +556,9 @@ def run_b200(args, cfg, rank, world, local_rank):
                                        f"pipelined: commit(k) on a side stream overlaps verify(k-1); "
                                        f"select/verify {args.ctas} CTAs/SM" if args.pipeline_on else
                                        "graph: serial step replayed as one CUDA graph" if args.schedule == "graph"
+                                       else f"pipegraph: select, commit and verify of different batches on three "
+                                            f"streams, all {args.steps} batches captured as one CUDA graph"
+                                       if args.schedule == "pipegraph"
                                        else "serial")},
             "cpu_baseline": cpu,
             "exact_mode": exact,
@@ -566,13 +588,16 @@ def main():
                     help="skip the exact-mode (reference algorithm) GPU measurement")
     ap.add_argument("--cpu-tokens", type=int, default=8192)
     ap.add_argument("--no-spot-check", dest="spot_check", action="store_false")
-    ap.add_argument("--schedule", default="auto", choices=["auto", "partition", "pipeline", "serial", "graph"],
-                    help="auto (default): partition from 512 chunks per GPU (AUTO_PIPELINE_MIN_CHUNKS), graph below; "
+    ap.add_argument("--schedule", default="auto",
+                    choices=["auto", "partition", "pipeline", "serial", "graph", "pipegraph"],
+                    help="auto (default): partition from 2048 chunks per GPU (AUTO_PIPELINE_MIN_CHUNKS), pipegraph below; "
                          "partition: the pipeline on two SM partitions (green contexts), commit on "
                          "--commit-sms SMs, select/verify on the rest; "
                          "pipeline: commit(k) on a side stream, co-resident with verify(k-1) and select(k+1); "
                          "serial: tl_select, tl_commit, tl_verify back to back; graph: the serial step "
-                         "captured as one CUDA graph (api.StepGraph) and replayed")
+                         "captured as one CUDA graph (api.StepGraph) and replayed; pipegraph: select, commit "
+                         "and verify of different batches on three streams (api.DualStreamPipeline), all K "
+                         "batches captured as one CUDA graph (api.PipelineGraph)")
     ap.add_argument("--commit-sms", type=int, default=24, help="SMs of the commitment partition (--schedule partition)")
     ap.add_argument("--pipeline", dest="schedule", action="store_const", const="pipeline")
     ap.add_argument("--partition", dest="schedule", action="store_const", const="partition")

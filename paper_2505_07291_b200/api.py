@@ -388,6 +388,34 @@ class StepGraph:
         return self.plan.rollout_accept
 
 
+class PipelineGraph:
+    """``len(provers)`` batches of a ``Pipeline`` captured as one CUDA graph.
+
+    For small batches every kernel is latency-bound and uses a fraction of the GPU, so
+    the pipeline's overlap (select(k+1) beside verify(k-1), commit(k) on the side stream)
+    runs the three stages of different batches concurrently, and the graph removes the
+    per-launch host cost.  ``replay()`` proves and verifies every captured batch and
+    returns their rollout-accept vectors; results are identical to the serial calls."""
+
+    def __init__(self, pipe: "Pipeline", provers, validators, thresholds: Thresholds = Thresholds()):
+        self.pipe = pipe
+        dev = pipe.eng.device
+        cur = torch.cuda.current_stream(dev)
+        warm = torch.cuda.Stream(dev)
+        warm.wait_stream(cur)
+        with torch.cuda.stream(warm):  # kernel attributes and allocations outside the capture
+            pipe.run(provers[:2], validators[:2], thresholds)
+        cur.wait_stream(warm)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.out = pipe.run(provers, validators, thresholds)
+
+    def replay(self) -> list[torch.Tensor]:
+        self.graph.replay()
+        return self.out
+
+
 class Pipeline:
     """Prove + verify a stream of equally-shaped batches with the commitment of batch
     k overlapping the verification of batch k-1.
@@ -520,7 +548,7 @@ class PartitionedPipeline(Pipeline):
                 side.wait_event(done)
                 if k >= 3:
                     side.wait_event(ver_done[k - 3])  # this plan's proofs read
-                self._commit(pl, k, side, False, on_commit, com_done)
+                self._commit(pl, k, side, self.co_resident, on_commit, com_done)
             if k >= 2:
                 j = k - 2
                 pl = self.plans[j % 3]
@@ -548,6 +576,25 @@ class PartitionedPipeline(Pipeline):
             self.close()
         except Exception:
             pass
+
+
+class DualStreamPipeline(PartitionedPipeline):
+    """The partitioned pipeline's schedule (select(k) and verify(k-2) on two streams,
+    commit(k-1) on a third, three rotating buffer sets) on ordinary streams of the whole
+    GPU, with the co-resident commitment.  For small batches, whose kernels each use a
+    fraction of the GPU, the three stages of different batches run concurrently; unlike
+    green-context streams these can be captured in one CUDA graph (``PipelineGraph``)."""
+
+    def __init__(self, eng: "ToplocEngine", row_offsets, H: int):
+        Pipeline.__init__(self, eng, row_offsets, H, ctas_per_sm=0)
+        self.plans.append(Plan(eng, row_offsets, H))
+        self.ws_verify = [torch.empty_like(p.ws) for p in self.plans]
+        self._handles = None
+        self.main = torch.cuda.Stream(eng.device)     # select
+        self.vstream = torch.cuda.Stream(eng.device)  # verify
+        self.side = torch.cuda.Stream(eng.device)     # commit
+        self.co_resident = True
+        self.sms = None
 
 
 _ENGINES: dict[tuple, ToplocEngine] = {}
