@@ -315,7 +315,7 @@ def run_b200(args, cfg, rank, world, local_rank):
     graph = api.StepGraph(plan, prv, val) if args.schedule == "graph" else None
     pgraph = None
     if args.schedule == "pipegraph":
-        pgraph_pipe = api.DualStreamPipeline(eng, offs, H)
+        pgraph_pipe = api.DualStreamPipeline(eng, offs, H, ctas_per_sm=args.pg_ctas)
         for _ in range(args.warmup):
             pgraph_pipe.run([prv], [val])
         pgraph = api.PipelineGraph(pgraph_pipe, [prv] * args.steps, [val] * args.steps)
@@ -605,6 +605,8 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak (default): every rank runs the configuration; strong: the configuration's "
                          "rollouts are sharded over the ranks by token count (scheduler.plan)")
+    ap.add_argument("--pg-ctas", type=int, default=0,
+                    help="select/verify CTAs per SM in the pipegraph schedule (0: full occupancy)")
     ap.add_argument("--ctas", type=int, default=16,
                     help="select/verify one-warp CTAs per SM in pipeline mode (leaves room for the commit CTA)")
     args = ap.parse_args()

@@ -585,8 +585,8 @@ class DualStreamPipeline(PartitionedPipeline):
     fraction of the GPU, the three stages of different batches run concurrently; unlike
     green-context streams these can be captured in one CUDA graph (``PipelineGraph``)."""
 
-    def __init__(self, eng: "ToplocEngine", row_offsets, H: int):
-        Pipeline.__init__(self, eng, row_offsets, H, ctas_per_sm=0)
+    def __init__(self, eng: "ToplocEngine", row_offsets, H: int, ctas_per_sm: int = 0):
+        Pipeline.__init__(self, eng, row_offsets, H, ctas_per_sm=ctas_per_sm)
         self.plans.append(Plan(eng, row_offsets, H))
         self.ws_verify = [torch.empty_like(p.ws) for p in self.plans]
         self._handles = None
