@@ -62,7 +62,7 @@ typedef struct tl_thresholds {
 } tl_thresholds;
 
 /* Per-chunk verification statistics (32 bytes). mean/median = +inf when no
- * exponent matches or the proof is invalid (p < 2). */
+ * exponent matches or the proof is invalid (p is not a prime in [32771, 65497]). */
 typedef struct tl_chunk_stats {
   uint32_t exp_mismatch;   /* points whose exponent field differs            */
   uint32_t n_match;        /* points whose exponent field agrees             */

@@ -39,8 +39,8 @@ Pinned semantics (DESIGN.md section 3 repeats them)
    exponent ``(v >> 7) & 0xFF``, mantissa ``v & 0x7F``; ``exp_mismatch`` counts
    exponent differences; mantissa |diff| over exponent-equal points gives
    ``mean = sum / n`` (f64) and ``median`` = ``statistics.median`` (average of
-   the two middle values).  No exponent-equal point, or ``p < 2`` in the proof:
-   mean = median = +inf.
+   the two middle values).  No exponent-equal point, or a proof modulus that is not
+   a prime in ``[32771, 65497]`` (a bad proof): mean = median = +inf.
 6. Chunk accepted iff ``exp_mismatch <= max_exp_mismatch and mean <=
    max_mant_mean and median <= max_mant_median``; a rollout is accepted iff all
    its chunks are.
@@ -69,6 +69,7 @@ def _primes_desc(lo: int = P_MIN, hi: int = P_MAX) -> list[int]:
 
 
 PRIMES_DESC = _primes_desc()
+PRIME_SET = frozenset(PRIMES_DESC)
 
 
 @dataclass(frozen=True)
@@ -333,7 +334,7 @@ def chunk_stats(claimed: np.ndarray, observed: np.ndarray, th: Thresholds) -> Ch
 def verify_chunk(bits_chunk, proof: bytes, K: int = 128, th: Thresholds = Thresholds()) -> ChunkStats:
     idx, vals = select_topk(bits_chunk, K)
     p, coeffs = parse_proof(proof, K)
-    if p < 2:
+    if p not in PRIME_SET:  # only a prover modulus is a proof (p = 2 would match any exponent)
         return ChunkStats(len(idx), 0, 0, math.inf, math.inf, False)
     claimed = eval_poly(coeffs % p, p, idx)
     observed = vals.astype(np.int64) % p

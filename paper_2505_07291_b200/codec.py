@@ -10,7 +10,9 @@ additionally requires ``commit_interval == 32`` because proofs are defined over
 
 ``encode`` turns a proof batch into per-rollout hex lists; ``decode`` validates and
 packs per-rollout hex lists back into the (n_chunks, 258) uint8 layout ``tl_verify``
-reads.  Errors raise ``ProofFormatError`` (a ``ValueError``, like the reference's
+reads; a modulus field that is neither 0 (unprovable chunk) nor a prime in
+[32771, 65497] is a format error, since such a "proof" (p = 2, say) would match
+any activations.  Errors raise ``ProofFormatError`` (a ``ValueError``, like the reference's
 ``RolloutSchemaError``) naming the rollout and item.
 """
 
@@ -97,7 +99,32 @@ def decode(commitments, n_tokens=None, interval: int = TOPLOC_INTERVAL) -> tuple
         r = int(np.searchsorted(np.cumsum(counts), bad, side="right"))
         raise ProofFormatError(f"rollout {r} item {bad - int(np.sum(counts[:r]))}: not hex") from None
     arr = np.frombuffer(blob, dtype=np.uint8).reshape(-1, PROOF_BYTES).copy()
+    p = arr[:, 0].astype(np.int64) << 8 | arr[:, 1]
+    bad = np.nonzero((p != 0) & ~_PROVER_MODULUS[p])[0]
+    if bad.size:
+        q = int(bad[0])
+        r = int(np.searchsorted(np.cumsum(counts), q, side="right"))
+        raise ProofFormatError(f"rollout {r} item {q - int(np.sum(counts[:r]))}: modulus {int(p[q])} is not a "
+                               f"prime in [{P_MIN}, {P_MAX}]")
     return arr, np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+
+
+P_MIN, P_MAX = 32771, 65497
+
+
+def _prover_moduli() -> np.ndarray:
+    """Mask over u16 values: True for the moduli a prover emits (primes in [P_MIN, P_MAX])."""
+    sieve = np.ones(1 << 16, dtype=bool)
+    sieve[:2] = False
+    for i in range(2, 256):
+        if sieve[i]:
+            sieve[i * i::i] = False
+    sieve[:P_MIN] = False
+    sieve[P_MAX + 1:] = False
+    return sieve
+
+
+_PROVER_MODULUS = _prover_moduli()
 
 
 def _is_hex(s: str) -> bool:
@@ -110,7 +137,7 @@ def _is_hex(s: str) -> bool:
 
 def modulus(proof_hex_or_bytes) -> int:
     """The proof's modulus field (big-endian u16): a prime in [32771, 65497], or 0 for an
-    unprovable chunk."""
+    unprovable chunk (``decode`` rejects anything else; ``tl_verify`` marks it a bad proof)."""
     b = bytes.fromhex(proof_hex_or_bytes) if isinstance(proof_hex_or_bytes, str) else bytes(proof_hex_or_bytes)
     return int.from_bytes(b[:2], "big")
 

@@ -129,6 +129,18 @@ struct ModP {
   }
 };
 
+// True iff p is one of the moduli a prover can emit: a prime in [32771, 65497]
+// (kPrimesDesc).  Warp-uniform binary search over the descending table.
+__device__ __forceinline__ bool prover_prime(uint32_t p) {
+  if (p < kPrimesDesc[TL_N_PRIMES - 1] || p > kPrimesDesc[0]) return false;
+  int lo = 0, hi = TL_N_PRIMES - 1;  // kPrimesDesc[lo] >= p >= kPrimesDesc[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (kPrimesDesc[mid] >= p) lo = mid; else hi = mid;
+  }
+  return kPrimesDesc[lo] == p || kPrimesDesc[hi] == p;
+}
+
 // Chunk j -> (rollout, first row, rows) by binary search over the chunk prefix.
 struct ChunkRef {
   int64_t row_start;
@@ -1095,7 +1107,9 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
 #pragma unroll
     for (int r = 0; r < 4; ++r) slot.mhist[lane + 32 * r] = 0;
     __syncwarp();
-    const bool bad = p < 2;
+    // a proof is only as strong as its modulus: anything but one of the prover's primes
+    // (p = 2 with zero coefficients would match every exponent) is a bad proof
+    const bool bad = !prover_prime(p);
     unsigned mism = 0, msum = 0, nmatch = 0;
     if (!bad) {
       const ModP m(p);
@@ -1191,14 +1205,17 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
   PROF_FLUSH();
 }
 
+// A rollout is accepted iff all its chunks are.  Chunks at or past the caller's
+// n_chunks were never verified (a miscounted call): they reject, so a miscount fails
+// closed instead of reading stale accept bytes.
 __global__ void rollout_verdict_kernel(const uint8_t* __restrict__ chunk_accept,
-                                       const int64_t* __restrict__ prefix, int n_roll,
+                                       const int64_t* __restrict__ prefix, int n_roll, int64_t n_chunks,
                                        uint8_t* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= n_roll) return;
   int ok = 1;
-  for (int64_t q = prefix[r] + lane; q < prefix[r + 1]; q += 32) ok &= chunk_accept[q] ? 1 : 0;
+  for (int64_t q = prefix[r] + lane; q < prefix[r + 1]; q += 32) ok &= (q < n_chunks && chunk_accept[q]) ? 1 : 0;
   ok = __all_sync(0xFFFFFFFFu, ok);
   if (lane == 0) out[r] = (uint8_t)ok;
 }
@@ -1904,7 +1921,7 @@ int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
                                                                          accept);
   }
   if (rollout_accept_out)
-    rollout_verdict_kernel<<<(n_roll + 7) / 8, 256, 0, st>>>(accept, prefix, n_roll, rollout_accept_out);
+    rollout_verdict_kernel<<<(n_roll + 7) / 8, 256, 0, st>>>(accept, prefix, n_roll, n_chunks, rollout_accept_out);
   return launch_status();
 }
 

@@ -27,6 +27,7 @@ equality then holds) or an empty list when they fail (reject("commitment")).
 from __future__ import annotations
 
 import contextvars
+import sys
 from dataclasses import dataclass
 
 import numpy as np
@@ -89,6 +90,11 @@ def install(mode: str = "exact", thresholds=None, backend=None) -> None:
     _saved[("swarm.validator.checks", "validate_file")] = checks.validate_file
     import swarm.validator as validator_pkg
     _saved[("swarm.validator", "validate_file")] = validator_pkg.validate_file
+    # swarm/node.py:30 binds validate_file by name at import: rebind it when it is already
+    # loaded (a later import reads the rebound swarm.validator attribute)
+    node = sys.modules.get("swarm.node")
+    if node is not None and hasattr(node, "validate_file"):
+        _saved[("swarm.node", "validate_file")] = node.validate_file
 
     if mode == "exact":
         def exact_commitments(hidden, k=32):
@@ -104,8 +110,11 @@ def install(mode: str = "exact", thresholds=None, backend=None) -> None:
 
     def verify_commitments(hidden, k=32):
         queue = _claimed.get()
-        if queue is None:   # called outside validate_file: behave like the prover
-            return prove_commitments(hidden, k)
+        if queue is None:
+            # only the wrapped validate_file sets the claimed proofs; re-proving here would
+            # turn TOPLOC's tolerance back into byte equality (honest workers rejected)
+            raise RuntimeError("TOPLOC validator commitment check called outside the installed "
+                               "validate_file (a module bound the original validate_file before install())")
         claimed = queue.pop(0)
         try:  # 516-char hex items, ceil(T / 32) of them (codec.py, files.py:184-186)
             arr, _ = codec.decode([claimed], n_tokens=[len(hidden)], interval=k)
@@ -144,6 +153,8 @@ def install(mode: str = "exact", thresholds=None, backend=None) -> None:
     checks.build_commitments = verify_commitments
     checks.validate_file = validate_file
     validator_pkg.validate_file = validate_file
+    if ("swarm.node", "validate_file") in _saved:
+        node.validate_file = validate_file
 
 
 def uninstall() -> None:

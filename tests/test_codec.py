@@ -13,7 +13,11 @@ from paper_2505_07291_b200 import codec
 
 
 def random_proofs(n, seed=0):
-    return np.random.default_rng(seed).integers(0, 256, size=(n, codec.PROOF_BYTES), dtype=np.uint8)
+    rng = np.random.default_rng(seed)
+    arr = rng.integers(0, 256, size=(n, codec.PROOF_BYTES), dtype=np.uint8)
+    p = rng.choice([65497, 65479, 32771, 0], size=n)       # prover moduli (0: unprovable chunk)
+    arr[:, 0], arr[:, 1] = p >> 8, p & 0xFF
+    return arr
 
 
 def test_encode_matches_bytes_hex_and_round_trips():
@@ -43,6 +47,16 @@ def test_encode_from_row_offsets_uses_the_32_token_rule():
 def test_decode_rejects_malformed_lists(bad, msg):
     with pytest.raises(codec.ProofFormatError, match=msg):
         codec.decode(bad, n_tokens=[32])
+
+
+@pytest.mark.parametrize("p", [1, 2, 97, 128, 32769, 32770, 65498, 65521, 65535])
+def test_decode_rejects_non_prover_moduli(p):
+    """Only 0 (unprovable chunk) or a prime in [32771, 65497] is a proof modulus; p = 2 with
+    zero coefficients would match any activations."""
+    good = (65497).to_bytes(2, "big").hex() + "00" * 256
+    forged = p.to_bytes(2, "big").hex() + "00" * 256
+    with pytest.raises(codec.ProofFormatError, match=f"item 1: modulus {p} "):
+        codec.decode([[good], [good, forged]], n_tokens=[32, 64])
 
 
 def test_interval_is_enforced():

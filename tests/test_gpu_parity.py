@@ -304,6 +304,45 @@ def test_verify_malformed_proofs():
     check_verify_against_oracle(bits, offs, bad2)
 
 
+@pytest.mark.parametrize("p", [2, 3, 97, 127, 128, 32769, 32770, 65499, 65521])
+def test_forged_modulus_proofs_are_bad_proofs(p):
+    """A proof is only as strong as its modulus.  With p <= 128 every claimed and observed
+    value is below 128, so all exponent fields are 0 and p = 2 with zero coefficients
+    would pass for any activations.  Every modulus that is not one of the
+    prover's primes in [32771, 65497] is a bad proof: rejected, stats at +inf."""
+    offs = [0, 64, 96]
+    bits = synth_bits(0, 96, 640, seed=11, dist=0)
+    forged = [p.to_bytes(2, "big") + b"\x00" * 256] * 3
+    vb, ost, over = check_verify_against_oracle(bits, offs, forged)
+    assert over == [False, False]
+    assert all((s["flags"] & 2) and math.isinf(s["mant_mean"]) for s in vb.stats_host())
+
+
+def test_rollout_verdict_fails_closed_on_short_chunk_count():
+    """A C-ABI caller that passes too small an n_chunks gets the uncovered chunks
+    rejected (they were never verified), not accepted from stale bytes."""
+    import ctypes
+    from paper_2505_07291_b200 import _ffi
+    lib = _ffi.load()
+    H, offs = 256, np.array([0, 64, 128], dtype=np.int64)
+    bits = synth_bits(0, 128, H, seed=5, dist=0)
+    h = torch.from_numpy(bits.view(np.int16)).cuda()
+    pf = gpu_prove(bits, offs).proofs
+    od = torch.from_numpy(offs).cuda()
+    need = int(lib.tl_workspace_bytes(2, 4, 128))
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    cacc = torch.ones(4, dtype=torch.uint8, device="cuda")       # stale "accept" bytes
+    racc = torch.zeros(2, dtype=torch.uint8, device="cuda")
+    th = api.Thresholds().to_c()
+    for n_chunks, want in ((4, [1, 1]), (2, [1, 0]), (0, [0, 0])):
+        cacc.fill_(1)
+        rc = lib.tl_verify(h.data_ptr(), od.data_ptr(), 2, 128, H, 32, 128, n_chunks, pf.data_ptr(), ctypes.byref(th),
+                           None, cacc.data_ptr(), racc.data_ptr(), ws.data_ptr(), ws.numel(), None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        assert racc.cpu().tolist() == want, n_chunks
+
+
 def test_api_argument_errors():
     eng = api.engine()
     x = torch.zeros((64, 128), dtype=torch.bfloat16, device="cuda")

@@ -106,6 +106,18 @@ def test_prove_verify_roundtrip_and_rejections():
     assert verdict == [False] and stats[0].n_match == 0 and math.isinf(stats[0].mant_mean)
 
 
+@pytest.mark.parametrize("p", [2, 3, 97, 128, 32769, 65521])
+def test_forged_small_or_composite_modulus_is_a_bad_proof(p):
+    """p = 2 with zero coefficients makes every claimed and observed value < 2, so all
+    exponents agree and the mantissa diffs are <= 1: without the modulus check it passes
+    for any activations.  Only the prover's primes are accepted."""
+    bits = synth_bits(0, 64, 96, seed=13)
+    forged = [[p.to_bytes(2, "big") + bytes(256)] * 2]
+    stats, verdict = TO.verify_proofs(bits, [0, 64], forged)
+    assert verdict == [False]
+    assert all(s.exp_mismatch == 128 and s.n_match == 0 and math.isinf(s.mant_median) for s in stats)
+
+
 def test_median_is_statistics_median():
     claimed = np.array([0x3F80, 0x3F81, 0x3F84, 0x3F88], dtype=np.int64)
     observed = np.array([0x3F80, 0x3F80, 0x3F80, 0x3F80], dtype=np.int64)

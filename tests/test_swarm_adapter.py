@@ -141,3 +141,28 @@ def test_toploc_mode_enforces_commit_interval(adapter):
                 -(-len(rec.output_tokens) // 16) - len(rec.commitments))
     v = validate(build_rollout_file(f, forge.key), ctx)
     assert (v.result, v.failed_check) == ("reject", "schema") and "commit_interval" in v.details
+
+
+def test_toploc_mode_rebinds_an_already_imported_node(adapter):
+    """swarm/node.py:30 binds validate_file by name at import.  When the node module was
+    imported before install(), its binding is rebound too (and restored afterwards), so
+    the node's validator runs the TOPLOC check instead of the original digest compare."""
+    import swarm.node as node
+    import swarm.validator.checks as checks
+    orig = node.validate_file
+    forge, ctx = fixtures()
+    adapter.install("toploc", backend=OracleBackend())
+    assert node.validate_file is checks.validate_file and node.validate_file is not orig
+    assert node.validate_file(forge.honest(2, 0), ctx).result == "accept"
+    adapter.uninstall()
+    assert node.validate_file is orig
+
+
+def test_toploc_validator_commitments_outside_validate_file_raise(adapter):
+    """The validator-side commitment function only has claimed proofs inside the wrapped
+    validate_file; anywhere else it raises instead of silently re-proving (which would
+    turn TOPLOC's tolerance back into byte equality)."""
+    import swarm.validator.checks as checks
+    adapter.install("toploc", backend=OracleBackend())
+    with pytest.raises(RuntimeError, match="outside the installed validate_file"):
+        checks.build_commitments(np.zeros((32, 8)), 32)
