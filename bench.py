@@ -120,110 +120,258 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU baseline (oracle port)
-def _cpu_worker(args):
-    """One worker = one rollout slice: oracle prove + verify (TOPLOC restatement)."""
-    (T, H, seed, start_evt, q) = args
-    os.environ["OMP_NUM_THREADS"] = "1"
-    import numpy as np
-    from oracle import toploc_oracle as TO
-    from oracle.synth_cpu import synth_bits
-    prv = np.concatenate([synth_bits(r, min(512, T - r), H, seed) for r in range(0, T, 512)])
-    val = np.concatenate([synth_bits(r, min(512, T - r), H, seed, jitter_thr=JITTER_THR, jitter_seed=seed + 1)
-                          for r in range(0, T, 512)])
-    offs = [0, T]
-    q.put(("ready", None))
-    start_evt.wait()
-    t0 = time.perf_counter()
-    tab, chunks = TO._chunks_of(prv, offs, CHUNK)
-    _, _, proofs = TO.prove_chunks(chunks, TOPK, batch=16)
-    stats, verdict = TO.verify_proofs(val, offs, [proofs], CHUNK, TOPK)
-    dt = time.perf_counter() - t0
-    q.put(("done", (dt, T, bool(verdict[0]))))
+def _cpu_pool_worker(kind, T, H, seed, cmd_q, res_q):
+    """One host core: holds one rollout's prover and validator states (generated once,
+    outside any timed region) and, per step command, proves and verifies it.
 
-
-def _cpu_exact_worker(args):
-    """One worker = one rollout slice through the reference's own exact-mode algorithm
-    (oracle/exact_oracle.py restates rollout.py:51-68): commitments from the prover's
-    states, then the validator's recompute and digest-list compare (checks.py:209-213)."""
-    (T, H, seed, start_evt, q) = args
+    kind "toploc": the TOPLOC restatement (oracle/toploc_oracle.py prove + verify).
+    kind "exact": the reference's own exact-mode algorithm (oracle/exact_oracle.py restates
+    rollout.py:51-68): commitments from the prover's states, then the validator's recompute
+    and digest-list compare (checks.py:209-213)."""
     os.environ["OMP_NUM_THREADS"] = "1"
     import numpy as np
     from oracle import exact_oracle as EO
+    from oracle import toploc_oracle as TO
     from oracle.synth_cpu import synth_bits
-    bits = np.concatenate([synth_bits(r, min(512, T - r), H, seed) for r in range(0, T, 512)])
-    hidden = (bits.astype(np.uint32) << 16).view(np.float32)
-    q.put(("ready", None))
-    start_evt.wait()
-    t0 = time.perf_counter()
-    claimed = EO.build_commitments(hidden, CHUNK)
-    ok = EO.build_commitments(hidden, CHUNK) == claimed
-    dt = time.perf_counter() - t0
-    q.put(("done", (dt, T, ok)))
-
-
-def cpu_sample(T: int, H: int, workers: int, steps: int = 1, warmup: int = 0, worker=None):
-    """Run `warmup + steps` rounds of `workers` parallel oracle prove+verify slices."""
-    ctx = mp.get_context("spawn")
-    results = []
-    for it in range(warmup + steps):
-        q = ctx.Queue()
-        evt = ctx.Event()
-        procs = [ctx.Process(target=worker or _cpu_worker, args=((T, H, 7 + it * 1000 + w, evt, q),))
-                 for w in range(workers)]
-        for p in procs:
-            p.start()
-        for _ in procs:  # a worker that dies raises queue.Empty here instead of hanging the bench
-            assert q.get(timeout=600)[0] == "ready"
+    prv = np.concatenate([synth_bits(r, min(512, T - r), H, seed) for r in range(0, T, 512)])
+    if kind == "toploc":
+        val = np.concatenate([synth_bits(r, min(512, T - r), H, seed, jitter_thr=JITTER_THR, jitter_seed=seed + 1)
+                              for r in range(0, T, 512)])
+        for p in TO.PRIMES_DESC[:8]:   # the port's inverse tables: built once, before any timing
+            TO._inv_table(p)
+    else:
+        hidden = (prv.astype(np.uint32) << 16).view(np.float32)
+    offs = [0, T]
+    res_q.put(("ready", None))
+    while cmd_q.get() is not None:
         t0 = time.perf_counter()
-        evt.set()
-        done = [q.get(timeout=1800)[1] for _ in procs]
-        wall = time.perf_counter() - t0
-        for p in procs:
-            p.join()
-        if it >= warmup:
-            results.append((wall, sum(d[1] for d in done), all(d[2] for d in done)))
-    wall = sum(r[0] for r in results)
-    toks = sum(r[1] for r in results)
-    return toks / wall, wall / len(results), all(r[2] for r in results)
+        if kind == "toploc":
+            _, chunks = TO._chunks_of(prv, offs, CHUNK)
+            _, _, proofs = TO.prove_chunks(chunks, TOPK, batch=16)
+            _, verdict = TO.verify_proofs(val, offs, [proofs], CHUNK, TOPK)
+            ok = bool(verdict[0])
+        else:
+            claimed = EO.build_commitments(hidden, CHUNK)
+            ok = EO.build_commitments(hidden, CHUNK) == claimed
+        res_q.put(("done", (time.perf_counter() - t0, T, ok)))
 
 
-def cpu_workers() -> int:
-    n = os.cpu_count() or 1
-    try:
+class CpuPool:
+    """`workers` host processes (one per core), each holding one T-token rollout of the
+    workload; a step = every worker proves and verifies its rollout once, wall-timed from
+    the go signal to the last result.  Data generation and the port's table set-up happen
+    once, at start, outside every timed step."""
+
+    def __init__(self, kind: str, T: int, H: int, workers: int, seed0: int = 7):
+        ctx = mp.get_context("spawn")
+        self.T, self.workers = T, workers
+        self.res_q = ctx.Queue()
+        self.cmd_qs = [ctx.Queue() for _ in range(workers)]
+        self.procs = [ctx.Process(target=_cpu_pool_worker, args=(kind, T, H, seed0 + w, self.cmd_qs[w], self.res_q),
+                                  daemon=True) for w in range(workers)]
+        for p in self.procs:
+            p.start()
+        for _ in self.procs:  # a worker that dies raises queue.Empty here instead of hanging the bench
+            assert self.res_q.get(timeout=900)[0] == "ready"
+
+    def step(self):
+        t0 = time.perf_counter()
+        for q in self.cmd_qs:
+            q.put(1)
+        done = [self.res_q.get(timeout=1800)[1] for _ in self.procs]
+        return time.perf_counter() - t0, sum(d[1] for d in done), all(d[2] for d in done)
+
+    def run(self, steps: int, warmup: int = 0):
+        """-> (tokens/s over the timed steps, mean wall per step, all accepted)."""
+        for _ in range(warmup):
+            self.step()
+        res = [self.step() for _ in range(steps)]
+        wall = sum(r[0] for r in res)
+        return sum(r[1] for r in res) / wall, wall / len(res), all(r[2] for r in res)
+
+    def close(self):
+        for q in self.cmd_qs:
+            q.put(None)
+        for p in self.procs:
+            p.join(timeout=30)
+
+
+def cpu_workers(T: int = 8192, H: int = 5120) -> int:
+    n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    try:  # each worker holds its rollout twice plus the port's intermediates
         import psutil
-        mem_gb = psutil.virtual_memory().available / 2 ** 30
-        n = min(n, max(1, int(mem_gb // 2)))
+        per_worker = 4 * T * H * 2 + (1 << 30)
+        n = min(n, max(1, int(psutil.virtual_memory().available * 0.6 // per_worker)))
     except Exception:
         pass
     return max(1, min(n, 64))
 
 
+def cpu_rollout_tokens(cfg) -> int:
+    """Tokens per CPU worker: a whole rollout, or an 8192-token slice of a longer one."""
+    return min(cfg["T"], 8192)
+
+
+def config_block(args, cfg, R, R_total, world):
+    """The workload description both arms print (the reference arm's step is a bounded
+    sample of it, described in its cpu_baseline.sample)."""
+    return {"workload": cfg["name"], "config": args.config, "rollouts_per_gpu": R, "rollouts_total": R_total,
+            "tokens_per_rollout": cfg["T"], "hidden": cfg["H"], "chunk": CHUNK, "topk": TOPK, "dist": args.dist,
+            "validator": "same states with 5% of elements +-1 ulp (GPU nondeterminism model)",
+            "l2": (f"inputs {2 * R * cfg['T'] * cfg['H'] * 2 / 1e9:.1f} GB per GPU >> 126 MB L2; no flush needed"
+                   if 2 * R * cfg["T"] * cfg["H"] * 2 > 4 * 126e6 else
+                   f"inputs {2 * R * cfg['T'] * cfg['H'] * 2 / 1e6:.1f} MB fit in the 126 MB L2 (latency-bound "
+                   f"configuration, not a roofline one); not flushed"),
+            "parallelism": f"rollout-sharded x{world}"}
+
+
+def cpu_baseline_block(cfg, steps: int, warmup: int, exact_steps: int = 1):
+    """The oracle port timed on this host's cores (one process per core, whole rollouts),
+    plus the reference's own exact-mode path on the same cores for scale."""
+    T, H = cpu_rollout_tokens(cfg), cfg["H"]
+    workers = cpu_workers(T, H)
+    pool = CpuPool("toploc", T, H, workers)
+    try:
+        tps, per_step, ok = pool.run(steps, warmup)
+    finally:
+        pool.close()
+    what = "whole" if T == cfg["T"] else f"{T}-token slices of"
+    out = {"value": tps, "unit": "tokens/s", "cores": workers, "kind": "port", "per_core": tps / workers,
+           "ms_per_step": per_step * 1e3, "steps": steps, "all_accepted": ok,
+           "sample": f"per step {workers} processes (one per host core) each prove+verify {what} {cfg['T']}-token "
+                     f"rollout(s) x H={H} with oracle/toploc_oracle.py; data and the port's inverse tables built "
+                     f"before timing"}
+    epool = CpuPool("exact", T, H, workers)
+    try:
+        etps, ewall, eok = epool.run(exact_steps, 1)
+    finally:
+        epool.close()
+    out["reference_exact_mode"] = {
+        "value": etps, "unit": "tokens/s", "cores": workers, "per_core": etps / workers, "digests_match": eok,
+        "sample": f"per step {workers} processes each run build_commitments + recompute-and-compare on {what} "
+                  f"{cfg['T']}-token rollout(s) x H={H} (oracle/exact_oracle.py, the reference's rollout.py:51-68 "
+                  f"and checks.py:209-213)"}
+    return out
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, cfg, rank, world):
+    """The reference's CPU path for this workload on the box's host cores (rank 0 only;
+    the reference has no TOPLOC code, so this is the oracle port, kind "port")."""
     if rank != 0:
         return
-    workers = cpu_workers()
-    T_slice = 1024
-    tps, per_step, ok = cpu_sample(T_slice, cfg["H"], workers, steps=args.steps, warmup=args.warmup)
+    cpu = cpu_baseline_block(cfg, args.steps, args.warmup)
+    n_gpus = max(world, args.gpus)
     line = {
-        "impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
-        "config": {"workload": cfg["name"], "hidden": cfg["H"], "chunk": CHUNK, "topk": TOPK,
-                   "sample": f"{workers} parallel slices of {T_slice} tokens x H={cfg['H']} per step"},
-        "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": workers, "kind": "port",
-                         "sample": f"{workers} x {T_slice}-token slices (hidden {cfg['H']}) per step, "
-                                   "oracle/toploc_oracle.py prove+verify, one process per core"},
-        "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "all_accepted": ok,
+        "impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": "tokens/s", "n_gpus": n_gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["ms_per_step"], "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+        "config": config_block(args, cfg, cfg["R"], cfg["R"] * n_gpus, n_gpus),
+        "cpu_baseline": cpu,
+        "e2e": {"value": cpu["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "all_accepted": cpu["all_accepted"],
     }
-    # the reference's own exact-mode path (rollout.py:51-68 + checks.py:209-213) on the same cores
-    etps, ewall, eok = cpu_sample(T_slice, cfg["H"], workers, steps=1, warmup=0, worker=_cpu_exact_worker)
-    line["cpu_baseline"]["reference_exact_mode"] = {
-        "value": etps, "unit": "tokens/s", "cores": workers, "digests_match": eok,
-        "sample": f"{workers} x {T_slice}-token slices: build_commitments + recompute-and-compare "
-                  "(oracle/exact_oracle.py)"}
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- host placement
+_AFFINITY0 = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+
+
+def pin_to_gpu_numa_node(dev) -> dict | None:
+    """Restrict this rank to the host cores of its GPU's NUMA node (sysfs local_cpulist), so
+    pinned host buffers allocated afterwards are first-touched on that node and the e2e
+    copies do not cross the socket interconnect.  Returns what was done, or None."""
+    import torch
+    try:
+        pr = torch.cuda.get_device_properties(dev)
+        bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        base = f"/sys/bus/pci/devices/{bus}"
+        with open(f"{base}/local_cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        node = -1
+        if os.path.exists(f"{base}/numa_node"):
+            with open(f"{base}/numa_node") as f:
+                node = int(f.read().strip())
+        cpus &= _AFFINITY0 or cpus
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+        return {"pci": bus, "numa_node": node, "cpus": len(cpus)}
+    except Exception:
+        return None
+
+
+def restore_affinity() -> None:
+    if _AFFINITY0 is not None:
+        try:
+            os.sched_setaffinity(0, _AFFINITY0)
+        except OSError:
+            pass
+
+
+# ----------------------------------------------------------------------------- parity spot check
+def spot_check(plan, T, H, seed, d, row0, n_random):
+    """Full-size parity on sampled chunks, outside the timed region: the first and last
+    chunk of the first, a middle and the last rollout plus `n_random` random chunks.
+    Each is re-derived on the CPU from the counter-based generator (prover and validator
+    states) and compared with the oracle: indices and value bits (select), proof bytes
+    (commit), exponent mismatches, match counts, mantissa sums, means, medians and chunk
+    verdicts (verify), and each sampled rollout's verdict against its chunks."""
+    import numpy as np
+    from oracle import toploc_oracle as TO
+    from oracle.synth_cpu import synth_bits
+    cpr = -(-T // CHUNK)
+    R = plan.n_roll
+    rng = np.random.default_rng(0)
+    js = set(rng.choice(plan.n_chunks, size=min(n_random, plan.n_chunks), replace=False).tolist())
+    for r in sorted({0, R // 2, R - 1}):
+        js.update((r * cpr, r * cpr + cpr - 1))
+    js = sorted(js)
+    got_p = plan.proofs.cpu().numpy()
+    got_i = plan.idx.cpu().numpy()
+    got_b = plan.bits.cpu().numpy().view(np.uint16)
+    st = plan.stats.cpu().numpy().view(_stats_dtype()).reshape(-1)
+    cacc = plan.chunk_accept.cpu().numpy()
+    racc = plan.rollout_accept.cpu().numpy()
+    prv, val = [], []
+    for j in js:
+        r, c = divmod(j, cpr)
+        r0 = row0 + r * T + c * CHUNK
+        rows = min(CHUNK, T - c * CHUNK)
+        prv.append(synth_bits(r0, rows, H, seed, d).reshape(-1))
+        val.append(synth_bits(r0, rows, H, seed, d, jitter_thr=JITTER_THR, jitter_seed=seed + 1).reshape(-1))
+    idxs, vals, proofs = TO.prove_chunks(prv, TOPK)
+    bad = {"select": [], "proof": [], "stats": [], "chunk_verdict": []}
+    for t, j in enumerate(js):
+        kk = len(idxs[t])
+        if not (np.array_equal(got_i[j, :kk], idxs[t]) and np.array_equal(got_b[j, :kk], vals[t])):
+            bad["select"].append(j)
+        if got_p[j].tobytes() != proofs[t]:
+            bad["proof"].append(j)
+        o = TO.verify_chunk(val[t], proofs[t], TOPK)
+        g = st[j]
+        if (int(g["exp_mismatch"]), int(g["n_match"]), int(g["mant_sum"]), float(g["mant_median"])) != \
+                (o.exp_mismatch, o.n_match, o.mant_sum, o.mant_median) or not (
+                float(g["mant_mean"]) == o.mant_mean):
+            bad["stats"].append(j)
+        if bool(cacc[j]) != o.accept or bool(g["flags"] & 1) != o.accept:
+            bad["chunk_verdict"].append(j)
+    roll_ok = all(bool(racc[r]) == bool(np.all(cacc[r * cpr:(r + 1) * cpr])) for r in sorted({0, R // 2, R - 1}))
+    return {"chunks_checked": len(js), "boundary_rollouts": sorted({0, R // 2, R - 1}),
+            "proofs_bit_exact": not bad["proof"], "select_bit_exact": not bad["select"],
+            "verify_stats_exact": not bad["stats"], "chunk_verdicts_match": not bad["chunk_verdict"],
+            "rollout_verdicts_consistent": roll_ok, "mismatches": {k: v[:8] for k, v in bad.items() if v},
+            "chunks_rejected": int(sum(1 for j in js if not cacc[j]))}
+
+
+def _stats_dtype():
+    from paper_2505_07291_b200.api import STATS_DTYPE
+    return STATS_DTYPE
 
 
 # ----------------------------------------------------------------------------- B200 arm
@@ -282,22 +430,12 @@ def run_b200(args, cfg, rank, world, local_rank):
     serial_ms = {k: sum(e[i].elapsed_time(e[i + 1]) for e in ser) / len(ser)
                  for i, k in enumerate(("select", "commit", "verify"))}
 
-    # spot-check bit-exactness at full size on sampled chunks (outside the timed region)
+    # parity at full size on sampled chunks (outside the timed region): every rollout's
+    # first and last chunk of a few rollouts plus random ones, proofs AND verify statistics
+    # and verdicts against the oracle, re-derived on the CPU from the counter-based generator
     spot = None
     if args.spot_check and rank == 0:
-        from oracle import toploc_oracle as TO
-        from oracle.synth_cpu import synth_bits
-        rng = np.random.default_rng(0)
-        js = sorted(rng.choice(plan.n_chunks, size=min(3, plan.n_chunks), replace=False).tolist())
-        got = plan.proofs.cpu().numpy()
-        okp = []
-        for j in js:
-            r0 = (j // (T // CHUNK)) * T + (j % (T // CHUNK)) * CHUNK
-            rows = min(CHUNK, T - (j % (T // CHUNK)) * CHUNK)
-            bits = synth_bits(r0, rows, H, seed, d)
-            _, _, pr = TO.prove_chunks([bits.reshape(-1)], TOPK)
-            okp.append(pr[0] == got[j].tobytes())
-        spot = {"chunks": js, "proofs_bit_exact": all(okp)}
+        spot = spot_check(plan, T, H, seed, d, row0, args.spot_chunks)
 
     if args.schedule == "auto":
         # small batches are latency-bound: one CUDA graph per step beats the pipelines
@@ -434,8 +572,9 @@ def run_b200(args, cfg, rank, world, local_rank):
     if args.e2e:
         Re = min(R, args.e2e_rollouts)
         rows = Re * T
-        hp = torch.empty((rows, H), dtype=torch.bfloat16).pin_memory()
-        hv = torch.empty((rows, H), dtype=torch.bfloat16).pin_memory()
+        numa = pin_to_gpu_numa_node(dev)   # pinned buffers first-touched on the GPU's NUMA node
+        hp = torch.empty((rows, H), dtype=torch.bfloat16, pin_memory=True)
+        hv = torch.empty((rows, H), dtype=torch.bfloat16, pin_memory=True)
         hp.copy_(prv[:rows].cpu())
         hv.copy_(val[:rows].cpu())
         offs_e = offs[:Re + 1]
@@ -463,7 +602,7 @@ def run_b200(args, cfg, rank, world, local_rank):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": world * rows / (float(te.item()) / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "rollouts_per_gpu": Re,
-               "h2d_gbs_per_gpu": h2d / (float(te.item()) / 1e3) / 1e9,
+               "h2d_gbs_per_gpu": h2d / (float(te.item()) / 1e3) / 1e9, "host_numa": numa,
                "note": "public API (ToplocEngine.prove/verify) from pinned host tensors; proofs and verdicts read "
                        "back; bound by the host link (h2d_gbs_per_gpu against ~55 GB/s for PCIe 5 x16)"}
 
@@ -509,30 +648,16 @@ def run_b200(args, cfg, rank, world, local_rank):
         del hx
 
     cpu = None
-    if args.cpu_baseline and rank == 0 and world == 1:
-        workers = cpu_workers()
-        tps, wall, ok = cpu_sample(args.cpu_tokens, H, workers, steps=1, warmup=0)
-        cpu = {"value": tps, "unit": "tokens/s", "cores": workers, "kind": "port",
-               "sample": f"{workers} parallel {args.cpu_tokens}-token slices x H={H} "
-                         f"(oracle/toploc_oracle.py prove+verify, one process per core), wall {wall:.1f}s"}
-        # the reference's own (exact-mode) path on the same cores, for scale
-        etps, ewall, eok = cpu_sample(4096, H, workers, steps=1, warmup=0, worker=_cpu_exact_worker)
-        cpu["reference_exact_mode"] = {
-            "value": etps, "unit": "tokens/s", "cores": workers, "per_core": etps / workers, "digests_match": eok,
-            "sample": f"{workers} parallel 4096-token slices x H={H}: build_commitments + recompute-and-compare "
-                      f"(oracle/exact_oracle.py, the reference's rollout.py:51-68), wall {ewall:.1f}s"}
+    if args.cpu_baseline and rank == 0:   # after the timed region; the other ranks wait at the final barrier
+        restore_affinity()
+        cpu = cpu_baseline_block(cfg, steps=1, warmup=1)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u16", "data": "synthetic",
-            "config": {"workload": cfg["name"], "config": args.config, "rollouts_per_gpu": R,
-                       "rollouts_total": R_total if shard is not None else world * R, "tokens_per_rollout": T,
-                       "hidden": H, "chunk": CHUNK, "topk": TOPK, "dist": args.dist,
-                       "validator": "same states with 5% of elements +-1 ulp (GPU nondeterminism model)",
-                       "l2": f"inputs {2 * n_rows * H * 2 / 1e9:.1f} GB per GPU >> 126 MB L2; no flush needed",
-                       "parallelism": f"rollout-sharded x{world}"},
+            "config": config_block(args, cfg, R, R_total if shard is not None else world * R, world),
             "roofline": {"bound": "hbm", "kernel": "prove_select_kernel (tl_select)", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": sel_bytes, "avg_launch_ms": kern_ms, "peak_source": peak_src,
@@ -564,11 +689,29 @@ def run_b200(args, cfg, rank, world, local_rank):
             "exact_mode": exact,
             "e2e": e2e,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "comm": ({"backend": "nccl", "nranks": world, "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                      "data_path_collectives": 0, "collective": "one all_gather of the per-rollout verdict bytes"}
+                     if world > 1 else None),
             "clocks": clk,
             "rollouts_accepted": f"{accepted}/{R}",
             "parity_spot_check": spot,
         }
         print(json.dumps(line), flush=True)
+
+
+def self_launch(n: int) -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # keep stdout to the one JSON line
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -588,6 +731,7 @@ def main():
                     help="skip the exact-mode (reference algorithm) GPU measurement")
     ap.add_argument("--cpu-tokens", type=int, default=8192)
     ap.add_argument("--no-spot-check", dest="spot_check", action="store_false")
+    ap.add_argument("--spot-chunks", type=int, default=64, help="random chunks in the full-size parity check")
     ap.add_argument("--schedule", default="auto",
                     choices=["auto", "partition", "pipeline", "serial", "graph", "pipegraph"],
                     help="auto (default): partition from 2048 chunks per GPU (AUTO_PIPELINE_MIN_CHUNKS), pipegraph below; "
@@ -614,8 +758,15 @@ def main():
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
 
+    if args.impl == "b200" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` without a launcher: re-execute under torch.distributed.run,
+        # one NCCL rank per GPU (NCCL's init lines, with the communicator's nranks, go to stderr)
+        sys.exit(self_launch(args.gpus))
+
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "b200" and world != args.gpus and rank == 0:
+        print(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}; running {world} ranks", file=sys.stderr)
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     cfg = dict(CONFIGS[args.config])
     if args.rollouts:

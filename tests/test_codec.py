@@ -3,8 +3,6 @@ interval rules (worker/files.py:37,184-186; validator/checks.py:211), and -- whe
 reference package is importable -- a round trip through the reference's own signed
 file writer and parser."""
 
-import os
-import sys
 
 import numpy as np
 import pytest
@@ -74,12 +72,9 @@ def test_modulus_field():
     assert codec.modulus(p) == 65497 and codec.modulus(p.hex()) == 65497
 
 
-REF = "/root/reference/pkg/src"
-
-
 def test_round_trip_through_reference_file_format():
-    if os.path.isdir(REF) and REF not in sys.path:
-        sys.path.append(REF)
+    from refpath import add_ref_to_path
+    add_ref_to_path()
     files = pytest.importorskip("swarm.worker.files")
     from swarm.keys import SigningKey
     key = SigningKey.from_seed(7, 0)

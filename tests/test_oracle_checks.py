@@ -3,8 +3,6 @@ check_termination / check_sampling (swarm/validator/checks.py:120-142), includin
 threshold boundaries (<= floor, > theta, < p_low).  CPU; skipped where the reference
 package is not importable."""
 
-import os
-import sys
 from types import SimpleNamespace
 
 import numpy as np
@@ -12,9 +10,9 @@ import pytest
 
 from oracle import checks_oracle as CO
 
-REF = "/root/reference/pkg/src"
-if os.path.isdir(REF) and REF not in sys.path:
-    sys.path.append(REF)
+from refpath import add_ref_to_path
+
+add_ref_to_path()
 
 
 def cases(seed=0, n=400):

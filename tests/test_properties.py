@@ -13,7 +13,10 @@ from paper_2505_07291_b200 import codec, scheduler
 @given(st.lists(st.integers(0, 40), min_size=1, max_size=12), st.integers(0, 2**31 - 1))
 def test_codec_round_trip(chunks_per_rollout, seed):
     n = sum(chunks_per_rollout)
-    arr = np.random.default_rng(seed).integers(0, 256, size=(n, codec.PROOF_BYTES), dtype=np.uint8)
+    rng = np.random.default_rng(seed)
+    arr = rng.integers(0, 256, size=(n, codec.PROOF_BYTES), dtype=np.uint8)
+    p = rng.choice(TO.PRIMES_DESC + [0], size=n)          # a prover modulus (0: unprovable chunk)
+    arr[:, 0], arr[:, 1] = p >> 8, p & 0xFF
     co = np.concatenate([[0], np.cumsum(chunks_per_rollout)])
     hexed = codec.encode(arr, chunk_offsets=co)
     assert [len(h) for h in hexed] == chunks_per_rollout
