@@ -22,6 +22,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/toploc_b200.h"
 #include "primes.inc"
 
@@ -1220,6 +1222,428 @@ __global__ void rollout_verdict_kernel(const uint8_t* __restrict__ chunk_accept,
   if (lane == 0) out[r] = (uint8_t)ok;
 }
 
+// ----------------------------------------------------------------------------- TMA-ring streaming (large batches)
+//
+// The large-batch select / verify path.  One CTA streams one chunk at a time: a producer
+// warp (one elected lane) moves the chunk through a ring of kRingStages x 32 KiB shared-
+// memory stages with TMA bulk copies (cp.async.bulk + mbarrier transaction counts), and
+// kRingConsumers consumer warps each scan an interleaved quarter of every stage with
+// the same 16x2-SIMD magnitude test as the per-warp kernels.  Two CTAs per SM, so the
+// chunk tail of one CTA (candidate merge, output or proof evaluation; ~2-5 us) overlaps
+// the other CTA's streaming, while the producer keeps prefetching the next chunk.
+//
+// Why: a bare-read probe on configuration 2's 21.5 GB (tools/lab/ctaprobe.cu,
+// profiles/r02_ctaprobe.txt) streams 7.53 TB/s through a CTA-wide 32 KiB ring against
+// 7.19 TB/s for the per-warp register double buffer of the one-warp-per-chunk kernels,
+// and 2 CTAs/SM x 3 x 32 KiB keep 7.44 TB/s with a 6 us per-chunk tail.
+//
+// Correctness is the per-warp invariant of select_chunk applied to each consumer warp's
+// quarter (every element of the quarter with key >= the warp's theta is buffered, and a
+// warp whose theta was raised by a compaction holds >= kk keys >= it), so the union of
+// the four buffers holds the chunk's top-kk once it holds >= kk keys; otherwise the
+// chunk is re-scanned from global memory with a lower threshold.  Each warp ranks its
+// buffer, and the four ranked lists are merged (bitonic, as for split chunks).
+constexpr int kRingConsumers = 4;
+constexpr int kRingThreads = 32 * (kRingConsumers + 1);
+constexpr int kRingStages = 3;
+constexpr int kRingStageBytes = 32768;
+constexpr int kRingStageVec = kRingStageBytes / 16;                   // 2048
+constexpr int kRingSub = kRingStageVec / (kRingConsumers * 32 * kSelU);  // 8-vector sub-tiles per lane and stage
+static_assert(kRingSub * kRingConsumers * 32 * kSelU == kRingStageVec, "stage split");
+constexpr int kRingQueue = 32 * kSelU + 8;
+constexpr int kRingCtasPerSm = 2;
+
+struct RingMeta {
+  long long j;  // chunk (-1: no more work)
+  int q, nst;   // stage q of nst
+  int len;      // bytes in this stage
+  int n;        // elements in the chunk
+};
+struct RingWarpSlot {
+  unsigned long long wbuf[kWarpCap];  // candidate keys; the warp's ranked list (128, zero-padded) at chunk end
+  int sidx[kRingQueue];               // queued flagged vectors (index within the stage)
+  int lst_n;
+};
+struct RingSmem {
+  uint4 ring[kRingStages][kRingStageVec];
+  RingWarpSlot w[kRingConsumers];
+  unsigned long long top[TL_MAX_K];  // verify: the chunk's ranked top-kk
+  uint16_t coef[TL_MAX_K];           // verify: claimed coefficients
+  unsigned mhist[128];               // verify: |mantissa diff| histogram
+  RingMeta meta[kRingStages];
+  uint64_t full[kRingStages], empty[kRingStages];
+  int cnt[kRingConsumers];           // candidates per consumer warp at the chunk end
+  int cmp[kRingConsumers];           // ... and whether its threshold was raised by a compaction
+  unsigned red[3];                   // verify: mismatches, mantissa sum, matches
+  unsigned proof_p;                  // verify: the proof's modulus
+  Spec sp;                           // speculation for the next chunk (warp 0 -> all)
+};
+constexpr size_t kRingSmem = (sizeof(RingSmem) + 127) & ~(size_t)127;
+
+__device__ __forceinline__ void ring_bar() {  // the consumer warps only (the producer never joins)
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kRingConsumers) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// Test the n queued vectors' elements (vector sidx[e >> 3] of src, bf16 e & 7) exactly and
+// append the survivors; elem0 is the flat index of src's first element.
+template <bool SMEM>
+__device__ __forceinline__ void ring_flush(const uint4* src, unsigned elem0, WarpScan& w, int n, int kk, int lane) {
+  const uint16_t* s16 = reinterpret_cast<const uint16_t*>(src);
+  const unsigned tkey = (unsigned)(w.theta >> 40);
+  for (int e0 = 0; e0 < 8 * n; e0 += 32) {
+    const int e = e0 + lane;
+    bool p = false;
+    unsigned long long key = 0;
+    if (e < 8 * n) {
+      const int off = 8 * w.sidx[e >> 3] + (e & 7);
+      const unsigned b = SMEM ? s16[off] : (unsigned)__ldg(s16 + off);
+      if ((b & 0x7FFFu) >= tkey) {
+        key = make_key(b, elem0 + (unsigned)off);
+        p = key >= w.theta;
+      }
+    }
+    warp_append(p, key, w.wb, w.cnt, w.theta, kk, lane);
+  }
+  __syncwarp();
+  if (lane == 0) *w.lst_n = 0;
+  __syncwarp();
+}
+
+// This warp's share of one stage-sized piece of the chunk (nvec 16-B vectors at src, in
+// shared memory for the ring or in global memory for a re-scan): vectors
+// g = (u * kRingConsumers + wid) * 32 + lane, processed as kRingSub tiles of kSelU per lane.
+// Every queued vector is tested before returning (a ring stage is released afterwards).
+template <bool SMEM>
+__device__ __forceinline__ void ring_scan(const uint4* __restrict__ src, int nvec, unsigned elem0, WarpScan& w,
+                                          int kk, int lane, int wid) {
+#pragma unroll 1
+  for (int h = 0; h < kRingSub; ++h) {
+    const int g0 = (h * kSelU * kRingConsumers + wid) * 32 + lane;
+    uint4 v[kSelU];
+#pragma unroll
+    for (int u = 0; u < kSelU; ++u) {
+      const int g = g0 + u * kRingConsumers * 32;
+      v[u] = g < nvec ? (SMEM ? src[g] : ld_stream(src + g)) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    const unsigned c2 = coarse_c2(w.theta, elem0 + 8u * (unsigned)(g0 - lane));
+    unsigned mu[kSelU];
+#pragma unroll
+    for (int u = 0; u < kSelU; ++u) mu[u] = hmaxabs2(hmaxabs2(v[u].x, v[u].y), hmaxabs2(v[u].z, v[u].w));
+    unsigned m = mu[0];
+#pragma unroll
+    for (int u = 1; u < kSelU; ++u) m = hmaxabs2(m, mu[u]);
+    const bool hit = coarse_hit(m, c2);
+    if (!__any_sync(0xFFFFFFFFu, hit)) continue;
+    if (hit) {
+      unsigned hm = 0;
+#pragma unroll
+      for (int u = 0; u < kSelU; ++u) hm |= ((g0 + u * kRingConsumers * 32 < nvec && coarse_hit(mu[u], c2)) ? 1u : 0u) << u;
+      if (hm) {
+        int pos = atomicAdd(w.lst_n, __popc(hm));
+#pragma unroll
+        for (int u = 0; u < kSelU; ++u)
+          if ((hm >> u) & 1u) w.sidx[pos++] = g0 + u * kRingConsumers * 32;
+      }
+    }
+    __syncwarp();
+    const int pending = *reinterpret_cast<volatile int*>(w.lst_n);
+    if (pending >= kFlushAt) ring_flush<SMEM>(src, elem0, w, pending, kk, lane);
+  }
+  const int pending = *reinterpret_cast<volatile int*>(w.lst_n);
+  if (pending > 0) ring_flush<SMEM>(src, elem0, w, pending, kk, lane);
+}
+
+// Rank this warp's buffer and leave its top-min(kk, cnt) in wb[0..128), zero-padded.
+__device__ __forceinline__ void ring_rank_own(unsigned long long* wb, int cnt, int lane) {
+  if (cnt <= 64) final_sort<2>(wb, cnt, lane);
+  else if (cnt <= 128) final_sort<4>(wb, cnt, lane);
+  else final_sort<8>(wb, cnt, lane);
+  for (int i = (cnt <= 64 ? 64 : 128) + lane; i < TL_MAX_K; i += 32) wb[i] = 0ull;
+  __syncwarp();
+}
+
+// Warp 0: merge the consumer warps' ranked lists into acc (the chunk's ranked top-128).
+__device__ __forceinline__ void ring_merge(const RingSmem& S, unsigned long long (&acc)[4], int lane) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) acc[r] = S.w[0].wbuf[32 * r + lane];
+#pragma unroll 1
+  for (int q = 1; q < kRingConsumers; ++q) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const unsigned long long b = S.w[q].wbuf[127 - (32 * r + lane)];
+      acc[r] = acc[r] > b ? acc[r] : b;
+    }
+    bitonic_merge_desc128(acc, lane);
+  }
+}
+
+// Producer: lane 0 of the last warp claims chunks (first round static, then the
+// workspace counter) and issues their stages into the ring.
+__device__ __forceinline__ void ring_produce(const SelArgs& a, RingSmem& S, int64_t n_chunks) {
+  int64_t j = blockIdx.x;
+  long long t = 0;
+  for (;;) {
+    const unsigned long long claim = j < n_chunks ? atomicAdd(a.next, 1ull) : 0ull;  // the next chunk, used next
+    if (j >= n_chunks) {
+      const int s = (int)(t % kRingStages);
+      if (t >= kRingStages) mbar_wait_parity(&S.empty[s], (unsigned)(((t / kRingStages) - 1) & 1));
+      S.meta[s].j = -1;
+      mbar_arrive(&S.full[s]);
+      return;
+    }
+    const ChunkGeo g = chunk_geo(a, j);
+    const int bytes = 2 * g.n;
+    const int nst = (bytes + kRingStageBytes - 1) / kRingStageBytes;
+    for (int q = 0; q < nst; ++q, ++t) {
+      const int s = (int)(t % kRingStages);
+      if (t >= kRingStages) mbar_wait_parity(&S.empty[s], (unsigned)(((t / kRingStages) - 1) & 1));
+      const int len = min(kRingStageBytes, bytes - q * kRingStageBytes);
+      S.meta[s] = RingMeta{(long long)j, q, nst, len, g.n};
+      mbar_expect_tx(&S.full[s], (uint32_t)len);
+      bulk_copy_g2s(S.ring[s], reinterpret_cast<const uint8_t*>(g.base) + (size_t)q * kRingStageBytes, (uint32_t)len,
+                    &S.full[s]);
+    }
+    j = (int64_t)gridDim.x + (int64_t)claim;
+  }
+}
+
+// Verify tail: evaluate the claimed polynomial at the chunk's ranked top-kk (one point per
+// consumer lane), compare exponents and mantissas, reduce, and write stats + verdict.
+__device__ __forceinline__ void ring_verify_tail(RingSmem& S, int64_t j, int kk, int K, const uint32_t (&pword)[5],
+                                                 const tl_thresholds& th, tl_chunk_stats* stats_out,
+                                                 uint8_t* accept_out, int lane, int wid) {
+  // warp 0 holds the proof words it loaded at the chunk start
+  unsigned p = 0;
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const int t = lane + 32 * q;
+      const unsigned v = ((pword[q] & 0xFFu) << 8) | (pword[q] >> 8);
+      if (t == 0) p = v;
+      else if (t <= TL_MAX_K) S.coef[t - 1] = (uint16_t)(t <= K ? v : 0u);
+    }
+    if (lane == 0) { S.proof_p = p; S.red[0] = 0u; S.red[1] = 0u; S.red[2] = 0u; }
+  }
+  for (int i = threadIdx.x; i < 128; i += 32 * kRingConsumers) S.mhist[i] = 0u;
+  ring_bar();
+  p = S.proof_p;
+  const bool bad = !prover_prime(p);
+  if (!bad) {
+    const ModP m(p);
+    const int i = 32 * wid + lane;
+    unsigned mism = 0, msum = 0, nmatch = 0;
+    if (i < kk) {
+      const unsigned long long key = S.top[i];
+      const uint32_t x = m.red(key_idx(key));
+      uint32_t acc = 0;
+      const uint4* c8 = reinterpret_cast<const uint4*>(S.coef);
+#pragma unroll 1
+      for (int kb = (K + 7) / 8 - 1; kb >= 0; --kb) {
+        const uint4 q = c8[kb];
+        const uint32_t cw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int e = 7; e >= 0; --e) acc = m.red(acc * x + ((cw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu));
+      }
+      const uint32_t obs = m.red((uint32_t)(key & 0xFFFFu));
+      if (((acc >> 7) & 0xFFu) != ((obs >> 7) & 0xFFu)) {
+        mism = 1;
+      } else {
+        const unsigned d = (unsigned)abs((int)(acc & 0x7Fu) - (int)(obs & 0x7Fu));
+        atomicAdd(&S.mhist[d], 1u);
+        msum = d;
+        nmatch = 1;
+      }
+    }
+    mism = __reduce_add_sync(0xFFFFFFFFu, mism);
+    msum = __reduce_add_sync(0xFFFFFFFFu, msum);
+    nmatch = __reduce_add_sync(0xFFFFFFFFu, nmatch);
+    if (lane == 0) {
+      atomicAdd(&S.red[0], mism);
+      atomicAdd(&S.red[1], msum);
+      atomicAdd(&S.red[2], nmatch);
+    }
+  }
+  ring_bar();
+  if (wid == 0) {
+    const unsigned mism = S.red[0], msum = S.red[1], nm = S.red[2];
+    unsigned c4[4], sum = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) { c4[t] = S.mhist[lane * 4 + t]; sum += c4[t]; }
+    unsigned incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    unsigned accb = incl - sum;
+    int v1 = -1, v2 = -1;
+    const unsigned q1 = nm ? (nm - 1) / 2 : 0, q2 = nm / 2;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (accb <= q1 && q1 < accb + c4[t]) v1 = lane * 4 + t;
+      if (accb <= q2 && q2 < accb + c4[t]) v2 = lane * 4 + t;
+      accb += c4[t];
+    }
+    v1 = __reduce_max_sync(0xFFFFFFFFu, v1);
+    v2 = __reduce_max_sync(0xFFFFFFFFu, v2);
+    if (lane == 0) {
+      tl_chunk_stats st;
+      if (bad) {
+        st.exp_mismatch = (uint32_t)kk; st.n_match = 0; st.mant_sum = 0;
+        st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
+        st.mant_median = st.mant_mean;
+        st.flags = TL_STAT_BADPROOF;
+      } else {
+        st.exp_mismatch = mism; st.n_match = nm; st.mant_sum = msum;
+        if (nm) {
+          st.mant_mean = (double)msum / (double)nm;
+          st.mant_median = ((double)v1 + (double)v2) * 0.5;
+        } else {
+          st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
+          st.mant_median = st.mant_mean;
+        }
+        const bool ok = (int)st.exp_mismatch <= th.max_exp_mismatch && st.mant_mean <= th.max_mant_mean &&
+                        st.mant_median <= th.max_mant_median;
+        st.flags = ok ? TL_STAT_ACCEPT : 0u;
+      }
+      if (stats_out) stats_out[j] = st;
+      accept_out[j] = (uint8_t)(st.flags & TL_STAT_ACCEPT);
+    }
+  }
+}
+
+template <bool VERIFY>
+__global__ void __launch_bounds__(kRingThreads, kRingCtasPerSm)
+ring_stream_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restrict__ bits_out,
+                   const uint8_t* __restrict__ proofs, tl_thresholds th, tl_chunk_stats* __restrict__ stats_out,
+                   uint8_t* __restrict__ accept_out) {
+  extern __shared__ __align__(128) uint8_t ring_smem[];
+  RingSmem& S = *reinterpret_cast<RingSmem*>(ring_smem);
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRingStages; ++s) {
+      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_addr(&S.full[s])), "r"(1));
+      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_addr(&S.empty[s])), "r"(kRingConsumers));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (lane == 0 && wid < kRingConsumers) S.w[wid].lst_n = 0;
+  __syncthreads();
+  const int64_t n_chunks = min(a.n_chunks, a.prefix[a.n_roll]);
+  if (wid == kRingConsumers) {
+    if (lane == 0) ring_produce(a, S, n_chunks);
+    return;
+  }
+  const int K = a.K, PB = 2 + 2 * K;
+  WarpScan w;
+  w.wb = S.w[wid].wbuf;
+  w.sidx = S.w[wid].sidx;
+  w.stg = nullptr;
+  w.lst_n = &S.w[wid].lst_n;
+  Spec sp = spec_load(a.spec, blockIdx.x);
+  uint32_t pword[5] = {0u, 0u, 0u, 0u, 0u};
+  unsigned long long theta0 = sp.theta;
+  for (long long t = 0;; ++t) {
+    const int s = (int)(t % kRingStages);
+    mbar_wait_parity(&S.full[s], (unsigned)((t / kRingStages) & 1));
+    const RingMeta m = S.meta[s];
+    if (m.j < 0) break;
+    const int kk = min(K, m.n);
+    if (m.q == 0) {
+      theta0 = sp.theta;
+      w.theta = theta0;
+      w.cnt = 0;
+      if (VERIFY && wid == 0) {  // this chunk's proof words, in flight while the chunk streams
+        const uint16_t* pw = reinterpret_cast<const uint16_t*>(proofs + m.j * PB);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          const int tt = lane + 32 * q;
+          pword[q] = tt <= K ? (uint32_t)__ldg(pw + tt) : 0u;
+        }
+      }
+    }
+    ring_scan<true>(S.ring[s], m.len >> 4, (unsigned)m.q * (kRingStageBytes / 2), w, kk, lane, wid);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[s]);
+    if (m.q != m.nst - 1) continue;
+
+    // ---- chunk tail (consumer warps only; the producer keeps filling the ring)
+    const int64_t j = m.j;
+    if (lane == 0) { S.cnt[wid] = w.cnt; S.cmp[wid] = w.theta != theta0; }
+    ring_bar();
+    int total = 0;
+#pragma unroll
+    for (int q = 0; q < kRingConsumers; ++q) total += S.cnt[q];
+    int retry = 0;
+    while (total < kk) {
+      // the speculative theta excluded part of the top-kk: re-scan the chunk from global
+      // memory with a lower threshold (64, then 256 magnitude steps, then 0)
+      if (theta0 == 0ull) __trap();  // unreachable: theta = 0 admits every element
+      const unsigned key = (unsigned)(theta0 >> 40);
+      const unsigned drop = retry == 0 ? 64u : 256u;
+      theta0 = (retry < 2 && key > drop) ? ((unsigned long long)(key - drop) << 40) : 0ull;
+      ++retry;
+      sp.delta = min(sp.delta + 4, 0x4000);
+      const ChunkGeo g = chunk_geo(a, j);
+      w.theta = theta0;
+      w.cnt = 0;
+      for (int q = 0; q < m.nst; ++q) {
+        const int len = min(kRingStageBytes, 2 * g.n - q * kRingStageBytes);
+        ring_scan<false>(reinterpret_cast<const uint4*>(g.base) + (size_t)q * kRingStageVec, len >> 4,
+                         (unsigned)q * (kRingStageBytes / 2), w, kk, lane, wid);
+      }
+      ring_bar();  // everyone has read the previous counts
+      if (lane == 0) { S.cnt[wid] = w.cnt; S.cmp[wid] = w.theta != theta0; }
+      ring_bar();
+      total = 0;
+#pragma unroll
+      for (int q = 0; q < kRingConsumers; ++q) total += S.cnt[q];
+    }
+    ring_rank_own(w.wb, w.cnt, lane);
+    ring_bar();
+    if (wid == 0) {
+      unsigned long long acc[4];
+      ring_merge(S, acc, lane);
+      // speculation for the CTA's next chunk (theta only rises by a compaction: too many candidates)
+      const unsigned long long kth = __shfl_sync(0xFFFFFFFFu, acc[(kk - 1) >> 5], (kk - 1) & 31);
+      bool compacted = false;
+#pragma unroll
+      for (int q = 0; q < kRingConsumers; ++q) compacted = compacted || S.cmp[q];
+      int d = sp.delta;
+      if ((total > kk + TL_SPEC_HI || compacted) && d > 1) --d;
+      else if (total < kk + TL_SPEC_LO) ++d;
+      sp.delta = d;
+      sp.k0 = sp.k1;
+      sp.k1 = (unsigned)(kth >> 40);
+      spec_arm(sp);
+      if (lane == 0) S.sp = sp;
+      if (VERIFY) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) S.top[32 * r + lane] = acc[r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int i = 32 * r + lane;
+          if (i < K) {
+            idx_out[j * K + i] = i < kk ? (int32_t)key_idx(acc[r]) : -1;
+            bits_out[j * K + i] = i < kk ? (uint16_t)(acc[r] & 0xFFFFu) : (uint16_t)0;
+          }
+        }
+      }
+    }
+    ring_bar();  // the merged lists are consumed before any warp refills its buffer
+    sp = S.sp;
+    if (VERIFY) {
+      ring_verify_tail(S, j, kk, K, pword, th, stats_out, accept_out, lane, wid);
+      ring_bar();
+    }
+  }
+  if (wid == 0) spec_store(a.spec, blockIdx.x, sp, lane);
+}
+
 // ----------------------------------------------------------------------------- record checks
 // One 256-thread CTA per record (grid-stride over records): termination
 // (checks.py:120-131), sampling (checks.py:134-142), commitment verdict, in the
@@ -1718,13 +2142,37 @@ SelPlan sel_plan(int64_t n_chunks, int64_t chunk_elems, const void* kernel, cuda
 
 int launch_status() { return cudaGetLastError() == cudaSuccess ? TL_OK : TL_ECUDA; }
 
+// cudaFuncSetAttribute once per kernel and device (a per-call attribute write costs host
+// time on the latency-bound small batches).  The cache is set-once, not mutable state
+// that affects results.
+template <auto KERNEL>
+int smem_attr_once(size_t bytes) {
+  static std::atomic<uint32_t> done{0u};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TL_ECUDA;
+  const uint32_t bit = 1u << (dev & 31);
+  if (done.load(std::memory_order_acquire) & bit) return TL_OK;
+  if (cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return TL_ECUDA;
+  done.fetch_or(bit, std::memory_order_acq_rel);
+  return TL_OK;
+}
+
+// The TMA-ring kernels take large batches of 16-B aligned chunks (H % 8 == 0 and an aligned
+// hidden pointer) when the caller leaves the launch shape to the library (ctas_per_sm == 0;
+// > 0 or < 0 selects the one-warp-per-chunk kernels, e.g. beside a co-resident commitment).
+constexpr int kRingMinRounds = 4;  // chunks per ring CTA, at least
+int ring_grid(const uint16_t* hidden, int H, int64_t n_chunks, int ctas_per_sm, cudaStream_t st) {
+  if (ctas_per_sm != 0 || H % 8 != 0 || (reinterpret_cast<uintptr_t>(hidden) & 15u)) return 0;
+  const int64_t grid = (int64_t)stream_sms(st) * kRingCtasPerSm;
+  return n_chunks >= grid * kRingMinRounds ? (int)grid : 0;
+}
+
 template <int WARPS, bool HALF>
 int launch_commit_t(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, const uint16_t* tables,
                     uint8_t* proofs, unsigned long long* next, cudaStream_t st) {
   const size_t smem = (size_t)(HALF ? kHalfTab : 65536) * 2 + (2 * 128 + kHashSlots) * WARPS * 4;
-  if (cudaFuncSetAttribute(commit_kernel<WARPS, HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return TL_ECUDA;
+  if (smem_attr_once<commit_kernel<WARPS, HALF>>(smem)) return TL_ECUDA;
   int grid = stream_sms(st);  // one CTA per SM of the stream's partition
   if ((int64_t)grid * WARPS > n_chunks) grid = (int)((n_chunks + WARPS - 1) / WARPS);
   commit_kernel<WARPS, HALF><<<grid, WARPS * 32, smem, st>>>(idx, bits, n_chunks, K, tables, proofs, next);
@@ -1803,11 +2251,15 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
                                           reinterpret_cast<unsigned long long*>(ws + L.next), part_cnt);
   SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
             reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
-  if (cudaFuncSetAttribute(prove_select_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kSelSmem) != cudaSuccess ||
-      cudaFuncSetAttribute(prove_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kSelSmem) != cudaSuccess)
+  if (const int rg = ring_grid(hidden, H, n_chunks, ctas_per_sm, st)) {
+    if (smem_attr_once<ring_stream_kernel<false>>(kRingSmem)) return TL_ECUDA;
+    ring_stream_kernel<false><<<rg, kRingThreads, kRingSmem, st>>>(a, idx_out, bits_out, nullptr, tl_thresholds{},
+                                                                   nullptr, nullptr);
+    return launch_status();
+  }
+  if (smem_attr_once<prove_select_kernel<false>>(kSelSmem) || smem_attr_once<prove_select_kernel<true>>(kSelSmem))
     return TL_ECUDA;
+  if (ctas_per_sm < 0) ctas_per_sm = 0;
   const SelPlan sp = sel_plan(n_chunks, (int64_t)C * H, (const void*)prove_select_kernel<false>, st, ctas_per_sm);
   a.split = sp.split;
   a.part = reinterpret_cast<unsigned long long*>(ws + L.part);
@@ -1904,16 +2356,22 @@ int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   if (n_chunks > 0) {
     SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
               reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
-    if (cudaFuncSetAttribute(verify_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(verify_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmem) !=
-            cudaSuccess)
+    const int rg = ring_grid(hidden, H, n_chunks, ctas_per_sm, st);
+    if (rg) {
+      if (smem_attr_once<ring_stream_kernel<true>>(kRingSmem)) return TL_ECUDA;
+    } else if (smem_attr_once<verify_kernel<false>>(kSelSmem) || smem_attr_once<verify_kernel<true>>(kSelSmem)) {
       return TL_ECUDA;
-    const SelPlan sp = sel_plan(n_chunks, (int64_t)C * H, (const void*)verify_kernel<false>, st, ctas_per_sm);
+    }
+    if (ctas_per_sm < 0) ctas_per_sm = 0;
+    const SelPlan sp = rg ? SelPlan{rg, 1}
+                          : sel_plan(n_chunks, (int64_t)C * H, (const void*)verify_kernel<false>, st, ctas_per_sm);
     a.split = sp.split;
     a.part = reinterpret_cast<unsigned long long*>(ws + L.part);
     a.part_cnt = part_cnt;
-    if (sp.split > 1)
+    if (rg)
+      ring_stream_kernel<true><<<rg, kRingThreads, kRingSmem, st>>>(a, nullptr, nullptr, proofs, *thresholds_host,
+                                                                    stats_out, accept);
+    else if (sp.split > 1)
       verify_kernel<true><<<sp.grid, kSelBlockThreads, kSelSmem, st>>>(a, proofs, *thresholds_host, stats_out,
                                                                         accept);
     else
@@ -2003,6 +2461,11 @@ int tl_partition_destroy(void** streams) {
 }
 
 int32_t tl_stream_sms(void* stream) { return stream_sms(static_cast<cudaStream_t>(stream)); }
+
+int32_t tl_ring_grid(const uint16_t* hidden, int32_t H, int64_t n_chunks, int32_t ctas_per_sm, void* stream) {
+  if (H < 1 || n_chunks < 0) return TL_EINVAL;
+  return ring_grid(hidden, H, n_chunks, ctas_per_sm, static_cast<cudaStream_t>(stream));
+}
 
 int tl_exact_chains(const void* hidden, int32_t dtype, const int64_t* row_off, int32_t n_roll, int32_t H, int32_t k,
                     const int64_t* digest_off, uint8_t* digests_out, void* stream) {
