@@ -112,12 +112,10 @@ int tl_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_
 /*
  * Launch-shape variants for pipelining a stream of batches (the commitment of
  * batch k on a second stream, beside verify of batch k-1 and select of k+1).
- * ctas_per_sm = 0 leaves the launch shape to the library: large batches of
- * 16-byte aligned chunks (H % 8 == 0) stream through the TMA-ring kernels (two
- * 160-thread CTAs per SM, tl_ring_grid), everything else through the
- * one-warp-per-chunk kernels at full occupancy (18 CTAs per SM).  ctas_per_sm > 0
- * caps the one-warp-CTA grid (16 leaves the registers for one commit CTA);
- * ctas_per_sm < 0 selects the one-warp kernels at full occupancy;
+ * ctas_per_sm = 0 (or -1) runs the one-warp-per-chunk kernels at full occupancy
+ * (18 CTAs per SM); > 0 caps that grid (16 leaves the registers for one commit CTA);
+ * -2 opts in to the TMA-ring kernels for large batches of 16-byte aligned chunks
+ * (H % 8 == 0; two 320-thread CTAs per SM, tl_ring_grid), with identical results;
  * co_resident = 1 runs the commitment with 8 warps (<= 64 registers) and a 64 KiB
  * half inverse table so that CTA fits beside them.  Results are identical.
  */
@@ -128,10 +126,11 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
 int tl_commit_ex(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_t K,
                  uint8_t* proofs_out, void* workspace, size_t workspace_bytes, int32_t co_resident,
                  void* stream);
-/* Grid of the TMA-ring kernels for this call shape, or 0 when the one-warp-per-chunk
- * kernels serve it (ctas_per_sm != 0, H % 8 != 0, an unaligned hidden pointer, or
- * fewer than 4 chunks per ring CTA). */
-int32_t tl_ring_grid(const uint16_t* hidden, int32_t H, int64_t n_chunks, int32_t ctas_per_sm, void* stream);
+/* Grid of the TMA-ring kernel for this call shape (verify = 0: tl_select_ex, 1:
+ * tl_verify_ex), or 0 when the one-warp-per-chunk kernels serve it (ctas_per_sm != -2,
+ * H % 8 != 0, an unaligned hidden pointer, or fewer than 4 chunks per ring CTA). */
+int32_t tl_ring_grid(const uint16_t* hidden, int32_t H, int64_t n_chunks, int32_t ctas_per_sm, int32_t verify,
+                     void* stream);
 int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
                  int32_t H, int32_t C, int32_t K, int64_t n_chunks, const uint8_t* proofs,
                  const tl_thresholds* thresholds_host, tl_chunk_stats* stats_out,

@@ -198,7 +198,6 @@ struct WarpSlot {
   int sidx[kStageVec];                // queued flagged vector ids
   uint4 stage[kStageVec];             // queued flagged vectors
   uint16_t coef[TL_MAX_K];            // verify: the claimed coefficients
-  unsigned mhist[128];                // verify: |mantissa diff| histogram
   int lst_n;                          // queue length
 };
 static_assert(offsetof(WarpSlot, stage) % 16 == 0 && offsetof(WarpSlot, coef) % 16 == 0, "slot alignment");
@@ -369,7 +368,7 @@ __device__ __forceinline__ void warp_bitonic_desc(T (&a)[NPER], int lane) {
 //     (mag - base) << 20 | (2^19 - 1 - idx) << 1 | sign,
 // which order like the 64-bit keys ((mag, idx) is unique, so the sign never
 // decides) at half the shuffles and compares; otherwise as 64-bit keys.
-template <int NPER>
+template <int NPER, int WMAX = NPER * 32>  // writes back wb[0 .. WMAX) only
 __device__ __forceinline__ void final_sort(unsigned long long* wb, int cnt, int lane) {
   unsigned long long a[NPER];
   unsigned lo = 0xFFFFu, hi = 0u, imax = 0u;
@@ -398,12 +397,14 @@ __device__ __forceinline__ void final_sort(unsigned long long* wb, int cnt, int 
     warp_bitonic_desc<uint32_t, NPER>(k, lane);
 #pragma unroll
     for (int r = 0; r < NPER; ++r)
-      wb[r * 32 + lane] = k[r] ? make_key(((k[r] & 1u) << 15) | (base + (k[r] >> 20)), 0x7FFFFu - ((k[r] >> 1) & 0x7FFFFu))
-                               : 0ull;
+      if (r * 32 < WMAX)
+        wb[r * 32 + lane] = k[r] ? make_key(((k[r] & 1u) << 15) | (base + (k[r] >> 20)), 0x7FFFFu - ((k[r] >> 1) & 0x7FFFFu))
+                                 : 0ull;
   } else {
     warp_bitonic_desc<unsigned long long, NPER>(a, lane);
 #pragma unroll
-    for (int r = 0; r < NPER; ++r) wb[r * 32 + lane] = a[r];
+    for (int r = 0; r < NPER; ++r)
+      if (r * 32 < WMAX) wb[r * 32 + lane] = a[r];
   }
   __syncwarp();
 }
@@ -1054,6 +1055,135 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
 }
 
 
+// One warp verifies one chunk from its ranked top-kk keys (top, shared memory): decode
+// the claimed coefficients (pword: this lane's big-endian u16 proof words t = lane + 32 q),
+// evaluate the polynomial at the kk indices (Horner, four points per lane), compare
+// exponent and mantissa bits with the observed values mod p, and write the chunk
+// statistics and verdict.  coef (TL_MAX_K u16, 16-B aligned) is the warp's shared
+// scratch.
+constexpr int kPW = (TL_MAX_K + 1 + 31) / 32;  // proof words per lane
+__device__ __forceinline__ void verify_tail_warp(const unsigned long long* top, int kk, int K, const uint32_t (&pword)[kPW],
+                                                 uint16_t* coef, const tl_thresholds& th,
+                                                 tl_chunk_stats* __restrict__ stats_out, uint8_t* __restrict__ accept_out,
+                                                 int64_t j, int lane) {
+  // claimed coefficients (big-endian u16) -> coef, zero-padded to TL_MAX_K
+  unsigned p = 0;
+#pragma unroll
+  for (int q = 0; q < kPW; ++q) {
+    const int t = lane + 32 * q;
+    const unsigned v = ((pword[q] & 0xFFu) << 8) | (pword[q] >> 8);
+    if (t == 0) p = v;
+    else if (t <= TL_MAX_K) coef[t - 1] = (uint16_t)(t <= K ? v : 0u);
+  }
+  p = __shfl_sync(0xFFFFFFFFu, p, 0);
+  __syncwarp();
+  // a proof is only as strong as its modulus: anything but one of the prover's primes
+  // (p = 2 with zero coefficients would match every exponent) is a bad proof
+  const bool bad = !prover_prime(p);
+  unsigned mism = 0, msum = 0, nmatch = 0;
+  uint32_t dv[4] = {0xFFu, 0xFFu, 0xFFu, 0xFFu};  // |mantissa diff| of each exponent-equal point, else 0xFF
+  if (!bad) {
+    const ModP m(p);
+    uint32_t x[4], acc[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = lane + 32 * r;
+      x[r] = i < kk ? m.red(key_idx(top[i])) : 0u;
+      acc[r] = 0u;
+    }
+    // P(x) = L(x) + x^64 U(x) over the zero-padded TL_MAX_K coefficients: eight independent
+    // 64-step Horner chains per lane instead of four 128-step ones (half the latency)
+    static_assert(TL_MAX_K == 128, "two 64-coefficient halves");
+    const uint4* c8 = reinterpret_cast<const uint4*>(coef);
+    uint32_t hi[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) hi[r] = 0u;
+#pragma unroll 1
+    for (int kb = 7; kb >= 0; --kb) {
+      const uint4 ql = c8[kb], qh = c8[kb + 8];
+      const uint32_t cl[4] = {ql.x, ql.y, ql.z, ql.w}, ch[4] = {qh.x, qh.y, qh.z, qh.w};
+#pragma unroll
+      for (int e = 7; e >= 0; --e) {
+        const uint32_t a_ = (cl[e >> 1] >> (16 * (e & 1))) & 0xFFFFu, b_ = (ch[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          acc[r] = m.red(acc[r] * x[r] + a_);
+          hi[r] = m.red(hi[r] * x[r] + b_);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      uint32_t x64 = x[r];
+#pragma unroll
+      for (int s = 0; s < 6; ++s) x64 = m.mul(x64, x64);
+      acc[r] = m.add(acc[r], m.mul(x64, hi[r]));
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = lane + 32 * r;
+      if (i < kk) {
+        const uint32_t obs = m.red((uint32_t)(top[i] & 0xFFFFu));
+        const uint32_t claimed = acc[r];
+        if (((claimed >> 7) & 0xFFu) != ((obs >> 7) & 0xFFu)) {
+          ++mism;
+        } else {
+          const unsigned d = (unsigned)abs((int)(claimed & 0x7Fu) - (int)(obs & 0x7Fu));
+          dv[r] = d;
+          msum += d;
+          ++nmatch;
+        }
+      }
+    }
+  }
+  mism = __reduce_add_sync(0xFFFFFFFFu, mism);
+  msum = __reduce_add_sync(0xFFFFFFFFu, msum);
+  const unsigned nm = __reduce_add_sync(0xFFFFFFFFu, nmatch);
+  __syncwarp();
+  // median (statistics.median: the mean of the two middle values): the value of 0-based
+  // rank q is the smallest t in [0, 127] with more than q diffs <= t -- a 7-step binary
+  // search of warp counts per rank
+  auto select_rank = [&](unsigned q) {
+    unsigned lo = 0u, hi = 127u;
+#pragma unroll 1
+    while (lo < hi) {
+      const unsigned mid = (lo + hi) >> 1;
+      unsigned le = 0u;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) le += dv[r] <= mid ? 1u : 0u;
+      if (__reduce_add_sync(0xFFFFFFFFu, le) > q) hi = mid;
+      else lo = mid + 1u;
+    }
+    return lo;
+  };
+  const unsigned q1 = nm ? (nm - 1) / 2 : 0, q2 = nm / 2;
+  const int v1 = (int)select_rank(q1), v2 = q2 == q1 ? v1 : (int)select_rank(q2);
+  if (lane == 0) {
+    tl_chunk_stats st;
+    if (bad) {
+      st.exp_mismatch = (uint32_t)kk; st.n_match = 0; st.mant_sum = 0;
+      st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
+      st.mant_median = st.mant_mean;
+      st.flags = TL_STAT_BADPROOF;
+    } else {
+      st.exp_mismatch = mism; st.n_match = nm; st.mant_sum = msum;
+      if (nm) {
+        st.mant_mean = (double)msum / (double)nm;
+        st.mant_median = ((double)v1 + (double)v2) * 0.5;
+      } else {
+        st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
+        st.mant_median = st.mant_mean;
+      }
+      const bool ok = (int)st.exp_mismatch <= th.max_exp_mismatch && st.mant_mean <= th.max_mant_mean &&
+                      st.mant_median <= th.max_mant_median;
+      st.flags = ok ? TL_STAT_ACCEPT : 0u;
+    }
+    if (stats_out) stats_out[j] = st;
+    accept_out[j] = (uint8_t)(st.flags & TL_STAT_ACCEPT);
+  }
+  __syncwarp();
+}
+
 // Verify: the warp selects its chunk's top-kk on the validator tensor, evaluates
 // the claimed polynomial at the kk indices (Horner, four points per lane),
 // compares exponent and mantissa bits with the observed values mod p, and writes
@@ -1071,7 +1201,6 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
   const int64_t nw = (int64_t)gridDim.x * kSelWarps;
   const int K = a.K;
   const int PB = 2 + 2 * K;
-  constexpr int kPW = (TL_MAX_K + 1 + 31) / 32;  // proof words per lane
   const int64_t gw = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5);
   Spec sp = spec_load(a.spec, gw);
   PROF_DECL;
@@ -1096,108 +1225,7 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
       select_chunk(g, kk, slot, sp, lane PROF_PASS);
     }
 
-    // claimed coefficients (big-endian u16) -> slot.coef, zero-padded to TL_MAX_K
-    unsigned p = 0;
-#pragma unroll
-    for (int q = 0; q < kPW; ++q) {
-      const int t = lane + 32 * q;
-      const unsigned v = ((pword[q] & 0xFFu) << 8) | (pword[q] >> 8);
-      if (t == 0) p = v;
-      else if (t <= TL_MAX_K) slot.coef[t - 1] = (uint16_t)(t <= K ? v : 0u);
-    }
-    p = __shfl_sync(0xFFFFFFFFu, p, 0);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) slot.mhist[lane + 32 * r] = 0;
-    __syncwarp();
-    // a proof is only as strong as its modulus: anything but one of the prover's primes
-    // (p = 2 with zero coefficients would match every exponent) is a bad proof
-    const bool bad = !prover_prime(p);
-    unsigned mism = 0, msum = 0, nmatch = 0;
-    if (!bad) {
-      const ModP m(p);
-      uint32_t x[4], acc[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int i = lane + 32 * r;
-        x[r] = i < kk ? m.red(key_idx(slot.wbuf[i])) : 0u;
-        acc[r] = 0u;
-      }
-      const uint4* c8 = reinterpret_cast<const uint4*>(slot.coef);
-      for (int kb = (K + 7) / 8 - 1; kb >= 0; --kb) {
-        const uint4 q = c8[kb];
-        const uint32_t cw[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int e = 7; e >= 0; --e) {
-          const uint32_t c = (cw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
-#pragma unroll
-          for (int r = 0; r < 4; ++r) acc[r] = m.red(acc[r] * x[r] + c);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int i = lane + 32 * r;
-        if (i < kk) {
-          const uint32_t obs = m.red((uint32_t)(slot.wbuf[i] & 0xFFFFu));
-          const uint32_t claimed = acc[r];
-          if (((claimed >> 7) & 0xFFu) != ((obs >> 7) & 0xFFu)) {
-            ++mism;
-          } else {
-            const unsigned d = (unsigned)abs((int)(claimed & 0x7Fu) - (int)(obs & 0x7Fu));
-            atomicAdd(&slot.mhist[d], 1u);
-            msum += d;
-            ++nmatch;
-          }
-        }
-      }
-    }
-    mism = __reduce_add_sync(0xFFFFFFFFu, mism);
-    msum = __reduce_add_sync(0xFFFFFFFFu, msum);
-    const unsigned nm = __reduce_add_sync(0xFFFFFFFFu, nmatch);
-    __syncwarp();
-    // median over the 128-bin histogram (statistics.median: mean of the two middle values)
-    unsigned c4[4], sum = 0;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) { c4[t] = slot.mhist[lane * 4 + t]; sum += c4[t]; }
-    unsigned incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    unsigned accb = incl - sum;
-    int v1 = -1, v2 = -1;
-    const unsigned q1 = nm ? (nm - 1) / 2 : 0, q2 = nm / 2;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      if (accb <= q1 && q1 < accb + c4[t]) v1 = lane * 4 + t;
-      if (accb <= q2 && q2 < accb + c4[t]) v2 = lane * 4 + t;
-      accb += c4[t];
-    }
-    v1 = __reduce_max_sync(0xFFFFFFFFu, v1);
-    v2 = __reduce_max_sync(0xFFFFFFFFu, v2);
-    if (lane == 0) {
-      tl_chunk_stats st;
-      if (bad) {
-        st.exp_mismatch = (uint32_t)kk; st.n_match = 0; st.mant_sum = 0;
-        st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
-        st.mant_median = st.mant_mean;
-        st.flags = TL_STAT_BADPROOF;
-      } else {
-        st.exp_mismatch = mism; st.n_match = nm; st.mant_sum = msum;
-        if (nm) {
-          st.mant_mean = (double)msum / (double)nm;
-          st.mant_median = ((double)v1 + (double)v2) * 0.5;
-        } else {
-          st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
-          st.mant_median = st.mant_mean;
-        }
-        const bool ok = (int)st.exp_mismatch <= th.max_exp_mismatch && st.mant_mean <= th.max_mant_mean &&
-                        st.mant_median <= th.max_mant_median;
-        st.flags = ok ? TL_STAT_ACCEPT : 0u;
-      }
-      if (stats_out) stats_out[j] = st;
-      accept_out[j] = (uint8_t)(st.flags & TL_STAT_ACCEPT);
-    }
+    verify_tail_warp(slot.wbuf, kk, K, pword, slot.coef, th, stats_out, accept_out, j, lane);
     __syncwarp();
     PROF_MARK(4);
     if (SPLIT) break;  // one part per warp
@@ -1224,295 +1252,503 @@ __global__ void rollout_verdict_kernel(const uint8_t* __restrict__ chunk_accept,
 
 // ----------------------------------------------------------------------------- TMA-ring streaming (large batches)
 //
-// The large-batch select / verify path.  One CTA streams one chunk at a time: a producer
-// warp (one elected lane) moves the chunk through a ring of kRingStages x 32 KiB shared-
-// memory stages with TMA bulk copies (cp.async.bulk + mbarrier transaction counts), and
-// kRingConsumers consumer warps each scan an interleaved quarter of every stage with
-// the same 16x2-SIMD magnitude test as the per-warp kernels.  Two CTAs per SM, so the
-// chunk tail of one CTA (candidate merge, output or proof evaluation; ~2-5 us) overlaps
-// the other CTA's streaming, while the producer keeps prefetching the next chunk.
+// The large-batch select / verify path, one persistent CTA per SM with three warp roles:
+//   * a producer warp moves one chunk at a time through a ring of kRingStages x 32 KiB
+//     shared-memory stages with TMA bulk copies (cp.async.bulk + mbarrier transaction
+//     counts), claiming chunks like the per-warp kernels (first round static, then the
+//     workspace counter);
+//   * kRingConsumers consumer warps each scan an interleaved share of every stage with the
+//     same 16x2-SIMD magnitude test as the per-warp kernels, buffer their candidates and,
+//     at the chunk end, rank their buffer and hand it to a finisher -- and go straight on
+//     to the next chunk (their candidate buffers are double-buffered by chunk parity);
+//   * kRingFinishers finisher warps (one per buffer parity) merge the consumers' ranked
+//     lists into the chunk's top-kk and write the indices and values (prove) or evaluate
+//     the proof and write statistics and verdicts (verify).
+// So nothing on the streaming side ever waits for a chunk tail.
 //
 // Why: a bare-read probe on configuration 2's 21.5 GB (tools/lab/ctaprobe.cu,
-// profiles/r02_ctaprobe.txt) streams 7.53 TB/s through a CTA-wide 32 KiB ring against
-// 7.19 TB/s for the per-warp register double buffer of the one-warp-per-chunk kernels,
-// and 2 CTAs/SM x 3 x 32 KiB keep 7.44 TB/s with a 6 us per-chunk tail.
+// profiles/r02_ctaprobe.txt) streams 7.53 TB/s through a 5 x 32 KiB ring with 16 consumer
+// warps per SM against 7.19 TB/s for the per-warp register double buffer of the
+// one-warp-per-chunk kernels.  A first ring kernel whose consumers ran the chunk tail
+// themselves (CTA barriers, two CTAs per SM) measured 7.8 us of tail per chunk and 5.4 TB/s.
 //
-// Correctness is the per-warp invariant of select_chunk applied to each consumer warp's
-// quarter (every element of the quarter with key >= the warp's theta is buffered, and a
-// warp whose theta was raised by a compaction holds >= kk keys >= it), so the union of
-// the four buffers holds the chunk's top-kk once it holds >= kk keys; otherwise the
-// chunk is re-scanned from global memory with a lower threshold.  Each warp ranks its
-// buffer, and the four ranked lists are merged (bitonic, as for split chunks).
-constexpr int kRingConsumers = 4;
-constexpr int kRingThreads = 32 * (kRingConsumers + 1);
-constexpr int kRingStages = 3;
-constexpr int kRingStageBytes = 32768;
-constexpr int kRingStageVec = kRingStageBytes / 16;                   // 2048
-constexpr int kRingSub = kRingStageVec / (kRingConsumers * 32 * kSelU);  // 8-vector sub-tiles per lane and stage
-static_assert(kRingSub * kRingConsumers * 32 * kSelU == kRingStageVec, "stage split");
-constexpr int kRingQueue = 32 * kSelU + 8;
-constexpr int kRingCtasPerSm = 2;
+// A lane whose elements pass the coarse test appends the passing elements itself (one
+// per lane per round, re-read from the stage in shared memory), with no queue.
+//
+// Correctness: every consumer warp starts a chunk from the same threshold theta0 (the
+// producer stamps it on the chunk's first stage), and each warp keeps the per-warp
+// invariant of select_chunk on its share (every element of the share with key >= the
+// warp's theta is buffered; a warp whose theta was raised by a compaction holds >= kk
+// keys >= it).  Then an element no warp buffered has >= kk buffered keys above it as soon
+// as the warps hold >= kk keys in total, so the merged top-kk of the ranked lists is the
+// chunk's top-kk; otherwise the finisher re-scans the chunk from global memory with a
+// lower threshold.
+#ifndef TL_RING_CONSUMERS
+#define TL_RING_CONSUMERS 8
+#endif
+#ifndef TL_RING_STAGES
+#define TL_RING_STAGES 3
+#endif
+#ifndef TL_RING_STAGE_KB
+#define TL_RING_STAGE_KB 28
+#endif
+#ifndef TL_RING_FINISHERS
+#define TL_RING_FINISHERS 1
+#endif
+#ifndef TL_RING_CTAS
+#define TL_RING_CTAS 2
+#endif
+#ifndef TL_RING_STATS
+#define TL_RING_STATS 0
+#endif
+#ifndef TL_RING_LAB
+#define TL_RING_LAB 0
+#endif
+#if TL_RING_STATS  // lab instrumentation: chunks, candidates, re-scans, compactions, finisher cycles
+__device__ unsigned long long g_ring_stats[8];
+__device__ unsigned g_ring_trace[1024][4];  // CTA 0: per chunk theta magnitude, total, delta, kth magnitude
+__device__ unsigned g_ring_trace_n;
+#endif
+constexpr int kRingConsumers = TL_RING_CONSUMERS;
+constexpr int kRingFinishers = TL_RING_FINISHERS;  // chunk c -> finisher c % kRingFinishers, buffer c & 1
+constexpr int kRingProducer = kRingConsumers + kRingFinishers;  // warp index
+constexpr int kRingThreads = 32 * (kRingProducer + 1);
+constexpr int kRingStages = TL_RING_STAGES;
+constexpr int kRingStageBytes = TL_RING_STAGE_KB * 1024;
+constexpr int kRingStageVec = kRingStageBytes / 16;
+constexpr int kRingStride = kRingConsumers * 32;                         // vectors between a lane's vectors
+constexpr int kRingTileU = kRingStageVec / kRingStride < kSelU ? kRingStageVec / kRingStride : kSelU;
+constexpr int kRingSub = kRingStageVec / (kRingStride * kRingTileU);     // tiles per lane and stage
+static_assert(kRingSub * kRingStride * kRingTileU == kRingStageVec && kRingTileU <= 8, "stage split");
+constexpr int kRingCap = TL_MAX_K + 32;  // per-warp candidate keys: a compaction keeps kk, one round adds <= 32
+constexpr int kRingCtasPerSm = TL_RING_CTAS;
 
 struct RingMeta {
-  long long j;  // chunk (-1: no more work)
-  int q, nst;   // stage q of nst
-  int len;      // bytes in this stage
-  int n;        // elements in the chunk
+  long long j;               // chunk (-1: no more work)
+  unsigned long long theta;  // the chunk's starting threshold (stamped on every stage)
+  int q, nst;                // stage q of nst
+  int len;                   // bytes in this stage
+  int n;                     // elements in the chunk
 };
-struct RingWarpSlot {
-  unsigned long long wbuf[kWarpCap];  // candidate keys; the warp's ranked list (128, zero-padded) at chunk end
-  int sidx[kRingQueue];               // queued flagged vectors (index within the stage)
-  int lst_n;
+struct RingJob {
+  long long j;  // chunk (-1: the finisher exits)
+  unsigned long long theta;
+  int kk, nst;
 };
 struct RingSmem {
   uint4 ring[kRingStages][kRingStageVec];
-  RingWarpSlot w[kRingConsumers];
-  unsigned long long top[TL_MAX_K];  // verify: the chunk's ranked top-kk
-  uint16_t coef[TL_MAX_K];           // verify: claimed coefficients
-  unsigned mhist[128];               // verify: |mantissa diff| histogram
+  unsigned long long wbuf[2][kRingConsumers][kRingCap];  // by chunk parity: candidates, then ranked lists
+  unsigned long long uni[kRingFinishers][kWarpCap];      // the union of a chunk's candidate buffers, ranked
+  uint16_t coef[kRingFinishers][TL_MAX_K];               // verify: claimed coefficients
   RingMeta meta[kRingStages];
-  uint64_t full[kRingStages], empty[kRingStages];
-  int cnt[kRingConsumers];           // candidates per consumer warp at the chunk end
-  int cmp[kRingConsumers];           // ... and whether its threshold was raised by a compaction
-  unsigned red[3];                   // verify: mismatches, mantissa sum, matches
-  unsigned proof_p;                  // verify: the proof's modulus
-  Spec sp;                           // speculation for the next chunk (warp 0 -> all)
+  uint64_t full[kRingStages], empty[kRingStages];        // ring stage filled / released
+  uint64_t ready[2], freed[2];                           // ranked lists handed over / merged
+  RingJob job[2];
+  int cnt[2][kRingConsumers];  // candidates per consumer warp at the chunk end
+  int cmp[2][kRingConsumers];  // ... and whether its threshold was raised by a compaction
+  unsigned long long theta_next;  // speculation for the next chunk (finishers -> producer)
+  Spec spec;                      // the CTA's speculation state, updated in chunk order ...
+  long long spec_seq;             // ... by the finisher of chunk spec_seq
 };
 constexpr size_t kRingSmem = (sizeof(RingSmem) + 127) & ~(size_t)127;
+static_assert(kRingCtasPerSm * (kRingSmem + 1024) <= 228 * 1024, "ring CTAs per SM");
 
-__device__ __forceinline__ void ring_bar() {  // the consumer warps only (the producer never joins)
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * kRingConsumers) : "memory");
-}
+struct RingScan {
+  unsigned long long theta;
+  int cnt;
+  unsigned long long* wb;
+};
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_init_count(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
 
-// Test the n queued vectors' elements (vector sidx[e >> 3] of src, bf16 e & 7) exactly and
-// append the survivors; elem0 is the flat index of src's first element.
-template <bool SMEM>
-__device__ __forceinline__ void ring_flush(const uint4* src, unsigned elem0, WarpScan& w, int n, int kk, int lane) {
-  const uint16_t* s16 = reinterpret_cast<const uint16_t*>(src);
-  const unsigned tkey = (unsigned)(w.theta >> 40);
-  for (int e0 = 0; e0 < 8 * n; e0 += 32) {
-    const int e = e0 + lane;
-    bool p = false;
-    unsigned long long key = 0;
-    if (e < 8 * n) {
-      const int off = 8 * w.sidx[e >> 3] + (e & 7);
-      const unsigned b = SMEM ? s16[off] : (unsigned)__ldg(s16 + off);
-      if ((b & 0x7FFFu) >= tkey) {
-        key = make_key(b, elem0 + (unsigned)off);
-        p = key >= w.theta;
-      }
-    }
-    warp_append(p, key, w.wb, w.cnt, w.theta, kk, lane);
+// Warp-uniform append of at most one key per lane into the warp's kRingCap buffer; a full
+// buffer keeps its kk largest keys and raises theta to the kk-th (rare path).
+__device__ __noinline__ unsigned long long ring_compact(unsigned long long* wb, int cnt, int kk, int lane) {
+  final_sort<kWarpCap / 32, TL_MAX_K>(wb, cnt, lane);
+  return wb[kk - 1];
+}
+__device__ __forceinline__ void ring_append(bool p, unsigned long long key, RingScan& w, int kk, int lane) {
+  unsigned bal = __ballot_sync(0xFFFFFFFFu, p);
+  if (!bal) return;
+  if (w.cnt + __popc(bal) > kRingCap) {
+    w.theta = ring_compact(w.wb, w.cnt, kk, lane);
+    w.cnt = kk;
+    p = p && key >= w.theta;
+    bal = __ballot_sync(0xFFFFFFFFu, p);
   }
-  __syncwarp();
-  if (lane == 0) *w.lst_n = 0;
+  if (p) w.wb[w.cnt + __popc(bal & lanemask_lt())] = key;
+  w.cnt += __popc(bal);
   __syncwarp();
 }
 
-// This warp's share of one stage-sized piece of the chunk (nvec 16-B vectors at src, in
-// shared memory for the ring or in global memory for a re-scan): vectors
-// g = (u * kRingConsumers + wid) * 32 + lane, processed as kRingSub tiles of kSelU per lane.
-// Every queued vector is tested before returning (a ring stage is released afterwards).
+// Coarse-test bits of one 16-B vector's 8 elements (bit e: |element e| >= the tile threshold).
+__device__ __forceinline__ uint32_t elem_mask8(const uint4& v, unsigned c2) {
+  const uint32_t f0 = ((v.x & 0x7FFF7FFFu) + c2) & 0x80008000u, f1 = ((v.y & 0x7FFF7FFFu) + c2) & 0x80008000u;
+  const uint32_t f2 = ((v.z & 0x7FFF7FFFu) + c2) & 0x80008000u, f3 = ((v.w & 0x7FFF7FFFu) + c2) & 0x80008000u;
+  return ((f0 >> 15) & 1u) | ((f0 >> 30) & 2u) | ((f1 >> 13) & 4u) | ((f1 >> 28) & 8u) | ((f2 >> 11) & 16u) |
+         ((f2 >> 26) & 32u) | ((f3 >> 9) & 64u) | ((f3 >> 24) & 128u);
+}
+
+// Share `wid` of one stage-sized piece of the chunk (nvec 16-B vectors at src, in shared
+// memory for the ring or in global memory for a re-scan): vectors
+// g = (u * kRingConsumers + wid) * 32 + lane, kRingTileU per lane per tile; elem0 is the
+// flat index of the piece's first element.
 template <bool SMEM>
-__device__ __forceinline__ void ring_scan(const uint4* __restrict__ src, int nvec, unsigned elem0, WarpScan& w,
+__device__ __forceinline__ void ring_scan(const uint4* __restrict__ src, int nvec, unsigned elem0, RingScan& w,
                                           int kk, int lane, int wid) {
+  const uint16_t* s16 = reinterpret_cast<const uint16_t*>(src);
 #pragma unroll 1
   for (int h = 0; h < kRingSub; ++h) {
-    const int g0 = (h * kSelU * kRingConsumers + wid) * 32 + lane;
-    uint4 v[kSelU];
+    const int g0 = (h * kRingTileU * kRingConsumers + wid) * 32 + lane;
+    uint4 v[kRingTileU];
 #pragma unroll
-    for (int u = 0; u < kSelU; ++u) {
-      const int g = g0 + u * kRingConsumers * 32;
+    for (int u = 0; u < kRingTileU; ++u) {
+      const int g = g0 + u * kRingStride;
       v[u] = g < nvec ? (SMEM ? src[g] : ld_stream(src + g)) : make_uint4(0u, 0u, 0u, 0u);
     }
     const unsigned c2 = coarse_c2(w.theta, elem0 + 8u * (unsigned)(g0 - lane));
-    unsigned mu[kSelU];
+    unsigned mu[kRingTileU];
 #pragma unroll
-    for (int u = 0; u < kSelU; ++u) mu[u] = hmaxabs2(hmaxabs2(v[u].x, v[u].y), hmaxabs2(v[u].z, v[u].w));
+    for (int u = 0; u < kRingTileU; ++u) mu[u] = hmaxabs2(hmaxabs2(v[u].x, v[u].y), hmaxabs2(v[u].z, v[u].w));
     unsigned m = mu[0];
 #pragma unroll
-    for (int u = 1; u < kSelU; ++u) m = hmaxabs2(m, mu[u]);
+    for (int u = 1; u < kRingTileU; ++u) m = hmaxabs2(m, mu[u]);
     const bool hit = coarse_hit(m, c2);
     if (!__any_sync(0xFFFFFFFFu, hit)) continue;
+    uint32_t em_lo = 0u, em_hi = 0u;  // element e of vector u: bit 8u + e (zero vectors past the end never hit)
     if (hit) {
-      unsigned hm = 0;
 #pragma unroll
-      for (int u = 0; u < kSelU; ++u) hm |= ((g0 + u * kRingConsumers * 32 < nvec && coarse_hit(mu[u], c2)) ? 1u : 0u) << u;
-      if (hm) {
-        int pos = atomicAdd(w.lst_n, __popc(hm));
-#pragma unroll
-        for (int u = 0; u < kSelU; ++u)
-          if ((hm >> u) & 1u) w.sidx[pos++] = g0 + u * kRingConsumers * 32;
+      for (int u = 0; u < kRingTileU; ++u) {
+        if (g0 + u * kRingStride < nvec && coarse_hit(mu[u], c2)) {
+          const uint32_t m8 = elem_mask8(v[u], c2);
+          if (u < 4) em_lo |= m8 << (8 * u);
+          else em_hi |= m8 << (8 * (u - 4));
+        }
       }
     }
-    __syncwarp();
-    const int pending = *reinterpret_cast<volatile int*>(w.lst_n);
-    if (pending >= kFlushAt) ring_flush<SMEM>(src, elem0, w, pending, kk, lane);
+    // one candidate element per lane per round, tested exactly against the composite key
+    for (;;) {
+      const bool has = (em_lo | em_hi) != 0u;
+      if (!__any_sync(0xFFFFFFFFu, has)) break;
+      bool p = false;
+      unsigned long long key = 0ull;
+      if (has) {
+        int bit;
+        if (em_lo) { bit = __ffs(em_lo) - 1; em_lo &= em_lo - 1u; }
+        else { bit = 31 + __ffs(em_hi); em_hi &= em_hi - 1u; }
+        const int off = 8 * (g0 + (bit >> 3) * kRingStride) + (bit & 7);  // element offset within src
+        const unsigned b = SMEM ? (unsigned)s16[off] : (unsigned)__ldg(s16 + off);
+        key = make_key(b, elem0 + (unsigned)off);
+        p = key >= w.theta;
+      }
+      ring_append(p, key, w, kk, lane);
+    }
   }
-  const int pending = *reinterpret_cast<volatile int*>(w.lst_n);
-  if (pending > 0) ring_flush<SMEM>(src, elem0, w, pending, kk, lane);
 }
 
-// Rank this warp's buffer and leave its top-min(kk, cnt) in wb[0..128), zero-padded.
-__device__ __forceinline__ void ring_rank_own(unsigned long long* wb, int cnt, int lane) {
-  if (cnt <= 64) final_sort<2>(wb, cnt, lane);
+// Rank a buffer and leave its top-min(128, cnt) in wb[0..128), zero-padded.
+__device__ __forceinline__ void ring_rank(unsigned long long* wb, int cnt, int lane) {
+  if (cnt <= 32) final_sort<1>(wb, cnt, lane);
+  else if (cnt <= 64) final_sort<2>(wb, cnt, lane);
   else if (cnt <= 128) final_sort<4>(wb, cnt, lane);
-  else final_sort<8>(wb, cnt, lane);
-  for (int i = (cnt <= 64 ? 64 : 128) + lane; i < TL_MAX_K; i += 32) wb[i] = 0ull;
+  else final_sort<8, TL_MAX_K>(wb, cnt, lane);
+  for (int i = (cnt <= 32 ? 32 : cnt <= 64 ? 64 : 128) + lane; i < TL_MAX_K; i += 32) wb[i] = 0ull;
   __syncwarp();
 }
 
-// Warp 0: merge the consumer warps' ranked lists into acc (the chunk's ranked top-128).
-__device__ __forceinline__ void ring_merge(const RingSmem& S, unsigned long long (&acc)[4], int lane) {
-#pragma unroll
-  for (int r = 0; r < 4; ++r) acc[r] = S.w[0].wbuf[32 * r + lane];
-#pragma unroll 1
-  for (int q = 1; q < kRingConsumers; ++q) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const unsigned long long b = S.w[q].wbuf[127 - (32 * r + lane)];
-      acc[r] = acc[r] > b ? acc[r] : b;
-    }
-    bitonic_merge_desc128(acc, lane);
+// Chunk j's geometry found by the whole (producer) warp: a 32-ary search over the chunk
+// prefix (two dependent loads for up to 1024 rollouts instead of ~10 for a binary search
+// by one thread), then the rollout's row range.
+__device__ __forceinline__ ChunkGeo warp_chunk_geo(const SelArgs& a, int64_t j, int lane) {
+  int lo = 0, hi = a.n_roll;  // prefix[lo] <= j < prefix[hi]
+  while (hi - lo > 1) {
+    const int step = (hi - lo + 31) >> 5;
+    const int idx = lo + lane * step;
+    const bool le = idx < hi && a.prefix[idx] <= j;
+    const int last = 31 - __clz(__ballot_sync(0xFFFFFFFFu, le));  // lane 0 (idx = lo) always holds
+    lo += last * step;
+    hi = min(hi, lo + step);
   }
+  const int64_t r0 = a.row_off[lo], T = a.row_off[lo + 1] - r0;
+  const int64_t local = j - a.prefix[lo];
+  ChunkGeo g;
+  g.base = a.hidden + (r0 + local * a.C) * (int64_t)a.H;
+  g.n = (int)min((int64_t)a.C, T - local * a.C) * a.H;
+  g.a0 = 0;  // ring chunks are 16-B aligned (ring_grid)
+  g.nvec = g.n >> 3;
+  g.nst = 0;
+  return g;
 }
 
-// Producer: lane 0 of the last warp claims chunks (first round static, then the
-// workspace counter) and issues their stages into the ring.
-__device__ __forceinline__ void ring_produce(const SelArgs& a, RingSmem& S, int64_t n_chunks) {
+// Producer warp: lane 0 issues the stages; the whole warp locates the next chunk while the
+// current one streams (the ring is full then, so the producer would only be waiting).
+__device__ __forceinline__ void ring_produce(const SelArgs& a, RingSmem& S, int64_t n_chunks, int lane) {
   int64_t j = blockIdx.x;
+  ChunkGeo g = warp_chunk_geo(a, j < n_chunks ? j : 0, lane);
   long long t = 0;
+  unsigned long long theta = 0ull;
+  auto issue = [&](int q, int nst, int bytes) {  // lane 0
+    const int s = (int)(t % kRingStages);
+    if (t >= kRingStages) mbar_wait_parity(&S.empty[s], (unsigned)(((t / kRingStages) - 1) & 1));
+    const int len = min(kRingStageBytes, bytes - q * kRingStageBytes);
+    S.meta[s] = RingMeta{(long long)j, theta, q, nst, len, g.n};
+    mbar_expect_tx(&S.full[s], (uint32_t)len);
+    bulk_copy_g2s(S.ring[s], reinterpret_cast<const uint8_t*>(g.base) + (size_t)q * kRingStageBytes, (uint32_t)len,
+                  &S.full[s]);
+    ++t;
+  };
   for (;;) {
-    const unsigned long long claim = j < n_chunks ? atomicAdd(a.next, 1ull) : 0ull;  // the next chunk, used next
     if (j >= n_chunks) {
-      const int s = (int)(t % kRingStages);
-      if (t >= kRingStages) mbar_wait_parity(&S.empty[s], (unsigned)(((t / kRingStages) - 1) & 1));
-      S.meta[s].j = -1;
-      mbar_arrive(&S.full[s]);
+      if (lane == 0) {
+        const int s = (int)(t % kRingStages);
+        if (t >= kRingStages) mbar_wait_parity(&S.empty[s], (unsigned)(((t / kRingStages) - 1) & 1));
+        S.meta[s].j = -1;
+        mbar_arrive(&S.full[s]);
+      }
       return;
     }
-    const ChunkGeo g = chunk_geo(a, j);
+    const unsigned long long claim = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;  // the next chunk
     const int bytes = 2 * g.n;
     const int nst = (bytes + kRingStageBytes - 1) / kRingStageBytes;
-    for (int q = 0; q < nst; ++q, ++t) {
-      const int s = (int)(t % kRingStages);
-      if (t >= kRingStages) mbar_wait_parity(&S.empty[s], (unsigned)(((t / kRingStages) - 1) & 1));
-      const int len = min(kRingStageBytes, bytes - q * kRingStageBytes);
-      S.meta[s] = RingMeta{(long long)j, q, nst, len, g.n};
-      mbar_expect_tx(&S.full[s], (uint32_t)len);
-      bulk_copy_g2s(S.ring[s], reinterpret_cast<const uint8_t*>(g.base) + (size_t)q * kRingStageBytes, (uint32_t)len,
-                    &S.full[s]);
+    if (lane == 0) {
+      theta = *reinterpret_cast<volatile unsigned long long*>(&S.theta_next);  // the finishers' latest hint
+      issue(0, nst, bytes);
     }
-    j = (int64_t)gridDim.x + (int64_t)claim;
+    __syncwarp();
+    const int64_t jn = (int64_t)gridDim.x + (int64_t)__shfl_sync(0xFFFFFFFFu, claim, 0);
+    const ChunkGeo gn = warp_chunk_geo(a, jn < n_chunks ? jn : 0, lane);
+    if (lane == 0)
+      for (int q = 1; q < nst; ++q) issue(q, nst, bytes);
+    __syncwarp();
+    j = jn;
+    g = gn;
   }
 }
 
-// Verify tail: evaluate the claimed polynomial at the chunk's ranked top-kk (one point per
-// consumer lane), compare exponents and mantissas, reduce, and write stats + verdict.
-__device__ __forceinline__ void ring_verify_tail(RingSmem& S, int64_t j, int kk, int K, const uint32_t (&pword)[5],
-                                                 const tl_thresholds& th, tl_chunk_stats* stats_out,
-                                                 uint8_t* accept_out, int lane, int wid) {
-  // warp 0 holds the proof words it loaded at the chunk start
-  unsigned p = 0;
-  if (wid == 0) {
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      const int t = lane + 32 * q;
-      const unsigned v = ((pword[q] & 0xFFu) << 8) | (pword[q] >> 8);
-      if (t == 0) p = v;
-      else if (t <= TL_MAX_K) S.coef[t - 1] = (uint16_t)(t <= K ? v : 0u);
+// Consumer warp `wid`: scan its share of every stage; at each chunk end rank its buffer,
+// hand it to the chunk's finisher and continue with the next chunk.
+__device__ __forceinline__ void ring_consume(RingSmem& S, int K, int lane, int wid) {
+  RingScan w;
+  w.theta = 0ull;
+  w.cnt = 0;
+  w.wb = S.wbuf[0][wid];
+  unsigned long long theta0 = 0ull;
+  long long c = -1;  // chunk sequence number of this CTA
+  for (long long t = 0;; ++t) {
+    const int s = (int)(t % kRingStages);
+    mbar_wait_parity(&S.full[s], (unsigned)((t / kRingStages) & 1));
+    const RingMeta m = S.meta[s];
+    if (m.j < 0) break;
+    const int kk = min(K, m.n);
+    if (m.q == 0) {
+      ++c;
+      const int b = (int)(c & 1);
+      if (c >= 2 && TL_RING_LAB != 2) mbar_wait_parity(&S.freed[b], (unsigned)(((c >> 1) - 1) & 1));  // c - 2 merged
+      w.wb = S.wbuf[b][wid];
+      theta0 = TL_RING_LAB == 2 ? (0x4050ull << 40) : m.theta;  // lab build 2: a fixed typical threshold, no finish
+      w.theta = theta0;
+      w.cnt = 0;
     }
-    if (lane == 0) { S.proof_p = p; S.red[0] = 0u; S.red[1] = 0u; S.red[2] = 0u; }
+#if TL_RING_LAB != 1  // lab build 1: the ring alone (no scan)
+    ring_scan<true>(S.ring[s], m.len >> 4, (unsigned)m.q * (kRingStageBytes / 2), w, kk, lane, wid);
+#endif
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[s]);
+    if (m.q != m.nst - 1 || TL_RING_LAB == 2) continue;
+    const int b = (int)(c & 1);
+    if (lane == 0) {
+      S.cnt[b][wid] = w.cnt;
+      S.cmp[b][wid] = w.theta != theta0;
+      if (wid == 0) S.job[b] = RingJob{m.j, theta0, kk, m.nst};
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.ready[b]);
   }
-  for (int i = threadIdx.x; i < 128; i += 32 * kRingConsumers) S.mhist[i] = 0u;
-  ring_bar();
-  p = S.proof_p;
-  const bool bad = !prover_prime(p);
-  if (!bad) {
-    const ModP m(p);
-    const int i = 32 * wid + lane;
-    unsigned mism = 0, msum = 0, nmatch = 0;
-    if (i < kk) {
-      const unsigned long long key = S.top[i];
-      const uint32_t x = m.red(key_idx(key));
-      uint32_t acc = 0;
-      const uint4* c8 = reinterpret_cast<const uint4*>(S.coef);
+  // no more chunks: release both finishers
+  if (TL_RING_LAB == 2) c = -1;
+  for (long long cc = c + 1; cc <= c + 2; ++cc) {
+    const int b = (int)(cc & 1);
+    if (cc >= 2 && TL_RING_LAB != 2) mbar_wait_parity(&S.freed[b], (unsigned)(((cc >> 1) - 1) & 1));
+    if (lane == 0) {
+      if (wid == 0) S.job[b].j = -1;
+      mbar_arrive(&S.ready[b]);
+    }
+    __syncwarp();
+  }
+}
+
+// Finisher f: the chunks c with c & 1 == f.  Merge the consumers' ranked lists (or, when
+// they hold fewer than kk keys, re-scan the chunk from global memory with a lower
+// threshold), update the speculation, then output (prove) or verify.
+template <bool VERIFY>
+__device__ __forceinline__ void ring_finish(const SelArgs& a, RingSmem& S, int f, int32_t* __restrict__ idx_out,
+                                            uint16_t* __restrict__ bits_out, const uint8_t* __restrict__ proofs,
+                                            const tl_thresholds& th, tl_chunk_stats* __restrict__ stats_out,
+                                            uint8_t* __restrict__ accept_out, int lane) {
+  const int K = a.K, PB = 2 + 2 * K;
+  for (long long cseq = f;; cseq += kRingFinishers) {
+    const int b = (int)(cseq & 1);  // the consumers' buffer parity of this chunk
+    mbar_wait_parity(&S.ready[b], (unsigned)((cseq >> 1) & 1));
+#if TL_RING_STATS
+    const long long t0 = clock64();
+#endif
+    const RingJob job = S.job[b];
+    if (job.j < 0) break;
+    const int64_t j = job.j;
+    const int kk = job.kk;
+    uint32_t pword[kPW];
+    if (VERIFY) {  // this chunk's proof words, in flight during the merge
+      const uint16_t* pw = reinterpret_cast<const uint16_t*>(proofs + j * PB);
+#pragma unroll
+      for (int q = 0; q < kPW; ++q) {
+        const int tt = lane + 32 * q;
+        pword[q] = tt <= K ? (uint32_t)__ldg(pw + tt) : 0u;
+      }
+    }
+    int total = 0;
+    bool compacted = false;
+#pragma unroll
+    for (int q = 0; q < kRingConsumers; ++q) {
+      total += S.cnt[b][q];
+      compacted = compacted || S.cmp[b][q];
+    }
+    unsigned long long acc[4];
+    int retry = 0;
+    bool released = false;
+    if (total >= kk && total <= kWarpCap) {
+      // the usual case: gather the consumers' candidates (slot p of the concatenation is
+      // key p - pre[w] of warp w) and rank the union once
+      int cw = lane < kRingConsumers ? S.cnt[b][lane] : 0, pre = cw;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, pre, o);
+        if (lane >= o) pre += y;
+      }
+      pre -= cw;  // exclusive prefix of the warps' counts, lane w
+      unsigned long long* uni = S.uni[f];
+#pragma unroll
+      for (int r = 0; r < kWarpCap / 32; ++r) {
+        const int pos = 32 * r + lane;
+        int w = 0;
+#pragma unroll
+        for (int q = 1; q < kRingConsumers; ++q) w += __shfl_sync(0xFFFFFFFFu, pre, q) <= pos ? 1 : 0;
+        const int off = pos - __shfl_sync(0xFFFFFFFFu, pre, w);
+        if (pos < total) uni[pos] = S.wbuf[b][w][off];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.freed[b]);  // the consumers may refill their buffers already
+      released = true;
+      final_sort<kWarpCap / 32, TL_MAX_K>(uni, total, lane);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = uni[32 * r + lane];
+    } else if (total >= kk) {
+      // more candidates than the union holds (compactions, heavy ties): rank every buffer
+      // and merge the ranked lists
 #pragma unroll 1
-      for (int kb = (K + 7) / 8 - 1; kb >= 0; --kb) {
-        const uint4 q = c8[kb];
-        const uint32_t cw[4] = {q.x, q.y, q.z, q.w};
+      for (int q = 0; q < kRingConsumers; ++q) ring_rank(S.wbuf[b][q], S.cnt[b][q], lane);
 #pragma unroll
-        for (int e = 7; e >= 0; --e) acc = m.red(acc * x + ((cw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu));
-      }
-      const uint32_t obs = m.red((uint32_t)(key & 0xFFFFu));
-      if (((acc >> 7) & 0xFFu) != ((obs >> 7) & 0xFFu)) {
-        mism = 1;
-      } else {
-        const unsigned d = (unsigned)abs((int)(acc & 0x7Fu) - (int)(obs & 0x7Fu));
-        atomicAdd(&S.mhist[d], 1u);
-        msum = d;
-        nmatch = 1;
-      }
-    }
-    mism = __reduce_add_sync(0xFFFFFFFFu, mism);
-    msum = __reduce_add_sync(0xFFFFFFFFu, msum);
-    nmatch = __reduce_add_sync(0xFFFFFFFFu, nmatch);
-    if (lane == 0) {
-      atomicAdd(&S.red[0], mism);
-      atomicAdd(&S.red[1], msum);
-      atomicAdd(&S.red[2], nmatch);
-    }
-  }
-  ring_bar();
-  if (wid == 0) {
-    const unsigned mism = S.red[0], msum = S.red[1], nm = S.red[2];
-    unsigned c4[4], sum = 0;
+      for (int r = 0; r < 4; ++r) acc[r] = S.wbuf[b][0][32 * r + lane];
+#pragma unroll 1
+      for (int q = 1; q < kRingConsumers; ++q) {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) { c4[t] = S.mhist[lane * 4 + t]; sum += c4[t]; }
-    unsigned incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    unsigned accb = incl - sum;
-    int v1 = -1, v2 = -1;
-    const unsigned q1 = nm ? (nm - 1) / 2 : 0, q2 = nm / 2;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      if (accb <= q1 && q1 < accb + c4[t]) v1 = lane * 4 + t;
-      if (accb <= q2 && q2 < accb + c4[t]) v2 = lane * 4 + t;
-      accb += c4[t];
-    }
-    v1 = __reduce_max_sync(0xFFFFFFFFu, v1);
-    v2 = __reduce_max_sync(0xFFFFFFFFu, v2);
-    if (lane == 0) {
-      tl_chunk_stats st;
-      if (bad) {
-        st.exp_mismatch = (uint32_t)kk; st.n_match = 0; st.mant_sum = 0;
-        st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
-        st.mant_median = st.mant_mean;
-        st.flags = TL_STAT_BADPROOF;
-      } else {
-        st.exp_mismatch = mism; st.n_match = nm; st.mant_sum = msum;
-        if (nm) {
-          st.mant_mean = (double)msum / (double)nm;
-          st.mant_median = ((double)v1 + (double)v2) * 0.5;
-        } else {
-          st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
-          st.mant_median = st.mant_mean;
+        for (int r = 0; r < 4; ++r) {
+          const unsigned long long bb = S.wbuf[b][q][127 - (32 * r + lane)];
+          acc[r] = acc[r] > bb ? acc[r] : bb;
         }
-        const bool ok = (int)st.exp_mismatch <= th.max_exp_mismatch && st.mant_mean <= th.max_mant_mean &&
-                        st.mant_median <= th.max_mant_median;
-        st.flags = ok ? TL_STAT_ACCEPT : 0u;
+        bitonic_merge_desc128(acc, lane);
       }
-      if (stats_out) stats_out[j] = st;
-      accept_out[j] = (uint8_t)(st.flags & TL_STAT_ACCEPT);
+    } else {
+      // the speculative theta excluded part of the top-kk: this warp re-scans the whole
+      // chunk from global memory (every consumer share) with a lower threshold -- 64, then
+      // 256 magnitude steps, then 0 -- using the first list as its buffer
+      unsigned long long theta0 = job.theta;
+      const ChunkGeo g = chunk_geo(a, j);
+      RingScan w;
+      w.wb = S.wbuf[b][0];
+      do {
+        if (theta0 == 0ull) __trap();  // unreachable: theta = 0 admits every element
+        const unsigned key = (unsigned)(theta0 >> 40);
+        const unsigned drop = retry == 0 ? 64u : 256u;
+        theta0 = (retry < 2 && key > drop) ? ((unsigned long long)(key - drop) << 40) : 0ull;
+        ++retry;
+        w.theta = theta0;
+        w.cnt = 0;
+        for (int q = 0; q < job.nst; ++q) {
+          const int len = min(kRingStageBytes, 2 * g.n - q * kRingStageBytes);
+          for (int ws = 0; ws < kRingConsumers; ++ws)
+            ring_scan<false>(reinterpret_cast<const uint4*>(g.base) + (size_t)q * kRingStageVec, len >> 4,
+                             (unsigned)q * (kRingStageBytes / 2), w, kk, lane, ws);
+        }
+      } while (w.cnt < kk);
+      total = w.cnt;
+      compacted = compacted || w.theta != theta0;
+      ring_rank(w.wb, w.cnt, lane);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = w.wb[32 * r + lane];
     }
+    // speculation, one CTA-wide state updated in chunk order by the two finishers (theta
+    // only rises by a compaction: a chunk with too many candidates)
+    const unsigned long long kth = __shfl_sync(0xFFFFFFFFu, acc[(kk - 1) >> 5], (kk - 1) & 31);
+    while (*reinterpret_cast<volatile long long*>(&S.spec_seq) != cseq) __nanosleep(64);  // leave the issue slots to the scans
+    Spec sp = S.spec;
+    int d = sp.delta;
+    if (retry) d = min(d + 4 * retry, 0x4000);
+    else if ((total > kk + TL_SPEC_HI || compacted) && d > 1) --d;
+    else if (total < kk + TL_SPEC_LO) ++d;
+    sp.delta = d;
+    sp.k0 = sp.k1;
+    sp.k1 = (unsigned)(kth >> 40);
+    spec_arm(sp);
+    __syncwarp();
+    if (lane == 0) {
+      S.spec = sp;
+      *reinterpret_cast<volatile unsigned long long*>(&S.theta_next) = sp.theta;
+      __threadfence_block();
+      *reinterpret_cast<volatile long long*>(&S.spec_seq) = cseq + 1;
+    }
+    if (VERIFY) {
+      __syncwarp();  // every lane has read the buffers: the union scratch now holds the ranked top-kk
+#pragma unroll
+      for (int r = 0; r < 4; ++r) S.uni[f][32 * r + lane] = acc[r];
+      __syncwarp();
+      verify_tail_warp(S.uni[f], kk, K, pword, S.coef[f], th, stats_out, accept_out, j, lane);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = 32 * r + lane;
+        if (i < K) {
+          idx_out[j * K + i] = i < kk ? (int32_t)key_idx(acc[r]) : -1;
+          bits_out[j * K + i] = i < kk ? (uint16_t)(acc[r] & 0xFFFFu) : (uint16_t)0;
+        }
+      }
+    }
+#if TL_RING_STATS
+    if (lane == 0 && blockIdx.x == 0) {
+      const unsigned n = atomicAdd(&g_ring_trace_n, 1u);
+      if (n < 1024) {
+        g_ring_trace[n][0] = (unsigned)(job.theta >> 40) | (unsigned)f << 31;
+        g_ring_trace[n][1] = (unsigned)total;
+        g_ring_trace[n][2] = (unsigned)d;
+        g_ring_trace[n][3] = (unsigned)(kth >> 40);
+      }
+    }
+    if (lane == 0) {
+      atomicAdd(&g_ring_stats[0], 1ull);
+      atomicAdd(&g_ring_stats[1], (unsigned long long)total);
+      atomicAdd(&g_ring_stats[2], (unsigned long long)retry);
+      atomicAdd(&g_ring_stats[3], compacted ? 1ull : 0ull);
+      atomicAdd(&g_ring_stats[4], (unsigned long long)(clock64() - t0));
+    }
+#endif
+    __syncwarp();
+    if (lane == 0 && !released) mbar_arrive(&S.freed[b]);
   }
+  if (f == 0) spec_store(a.spec, blockIdx.x, S.spec, lane);
 }
 
 template <bool VERIFY>
@@ -1525,123 +1761,24 @@ ring_stream_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restric
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRingStages; ++s) {
-      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_addr(&S.full[s])), "r"(1));
-      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_addr(&S.empty[s])), "r"(kRingConsumers));
+      mbar_init_count(&S.full[s], 1);
+      mbar_init_count(&S.empty[s], kRingConsumers);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init_count(&S.ready[b], kRingConsumers);
+      mbar_init_count(&S.freed[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    S.spec = spec_load(a.spec, blockIdx.x);
+    S.spec_seq = 0;
+    S.theta_next = S.spec.theta;
   }
-  if (lane == 0 && wid < kRingConsumers) S.w[wid].lst_n = 0;
   __syncthreads();
   const int64_t n_chunks = min(a.n_chunks, a.prefix[a.n_roll]);
-  if (wid == kRingConsumers) {
-    if (lane == 0) ring_produce(a, S, n_chunks);
-    return;
-  }
-  const int K = a.K, PB = 2 + 2 * K;
-  WarpScan w;
-  w.wb = S.w[wid].wbuf;
-  w.sidx = S.w[wid].sidx;
-  w.stg = nullptr;
-  w.lst_n = &S.w[wid].lst_n;
-  Spec sp = spec_load(a.spec, blockIdx.x);
-  uint32_t pword[5] = {0u, 0u, 0u, 0u, 0u};
-  unsigned long long theta0 = sp.theta;
-  for (long long t = 0;; ++t) {
-    const int s = (int)(t % kRingStages);
-    mbar_wait_parity(&S.full[s], (unsigned)((t / kRingStages) & 1));
-    const RingMeta m = S.meta[s];
-    if (m.j < 0) break;
-    const int kk = min(K, m.n);
-    if (m.q == 0) {
-      theta0 = sp.theta;
-      w.theta = theta0;
-      w.cnt = 0;
-      if (VERIFY && wid == 0) {  // this chunk's proof words, in flight while the chunk streams
-        const uint16_t* pw = reinterpret_cast<const uint16_t*>(proofs + m.j * PB);
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-          const int tt = lane + 32 * q;
-          pword[q] = tt <= K ? (uint32_t)__ldg(pw + tt) : 0u;
-        }
-      }
-    }
-    ring_scan<true>(S.ring[s], m.len >> 4, (unsigned)m.q * (kRingStageBytes / 2), w, kk, lane, wid);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.empty[s]);
-    if (m.q != m.nst - 1) continue;
-
-    // ---- chunk tail (consumer warps only; the producer keeps filling the ring)
-    const int64_t j = m.j;
-    if (lane == 0) { S.cnt[wid] = w.cnt; S.cmp[wid] = w.theta != theta0; }
-    ring_bar();
-    int total = 0;
-#pragma unroll
-    for (int q = 0; q < kRingConsumers; ++q) total += S.cnt[q];
-    int retry = 0;
-    while (total < kk) {
-      // the speculative theta excluded part of the top-kk: re-scan the chunk from global
-      // memory with a lower threshold (64, then 256 magnitude steps, then 0)
-      if (theta0 == 0ull) __trap();  // unreachable: theta = 0 admits every element
-      const unsigned key = (unsigned)(theta0 >> 40);
-      const unsigned drop = retry == 0 ? 64u : 256u;
-      theta0 = (retry < 2 && key > drop) ? ((unsigned long long)(key - drop) << 40) : 0ull;
-      ++retry;
-      sp.delta = min(sp.delta + 4, 0x4000);
-      const ChunkGeo g = chunk_geo(a, j);
-      w.theta = theta0;
-      w.cnt = 0;
-      for (int q = 0; q < m.nst; ++q) {
-        const int len = min(kRingStageBytes, 2 * g.n - q * kRingStageBytes);
-        ring_scan<false>(reinterpret_cast<const uint4*>(g.base) + (size_t)q * kRingStageVec, len >> 4,
-                         (unsigned)q * (kRingStageBytes / 2), w, kk, lane, wid);
-      }
-      ring_bar();  // everyone has read the previous counts
-      if (lane == 0) { S.cnt[wid] = w.cnt; S.cmp[wid] = w.theta != theta0; }
-      ring_bar();
-      total = 0;
-#pragma unroll
-      for (int q = 0; q < kRingConsumers; ++q) total += S.cnt[q];
-    }
-    ring_rank_own(w.wb, w.cnt, lane);
-    ring_bar();
-    if (wid == 0) {
-      unsigned long long acc[4];
-      ring_merge(S, acc, lane);
-      // speculation for the CTA's next chunk (theta only rises by a compaction: too many candidates)
-      const unsigned long long kth = __shfl_sync(0xFFFFFFFFu, acc[(kk - 1) >> 5], (kk - 1) & 31);
-      bool compacted = false;
-#pragma unroll
-      for (int q = 0; q < kRingConsumers; ++q) compacted = compacted || S.cmp[q];
-      int d = sp.delta;
-      if ((total > kk + TL_SPEC_HI || compacted) && d > 1) --d;
-      else if (total < kk + TL_SPEC_LO) ++d;
-      sp.delta = d;
-      sp.k0 = sp.k1;
-      sp.k1 = (unsigned)(kth >> 40);
-      spec_arm(sp);
-      if (lane == 0) S.sp = sp;
-      if (VERIFY) {
-#pragma unroll
-        for (int r = 0; r < 4; ++r) S.top[32 * r + lane] = acc[r];
-      } else {
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int i = 32 * r + lane;
-          if (i < K) {
-            idx_out[j * K + i] = i < kk ? (int32_t)key_idx(acc[r]) : -1;
-            bits_out[j * K + i] = i < kk ? (uint16_t)(acc[r] & 0xFFFFu) : (uint16_t)0;
-          }
-        }
-      }
-    }
-    ring_bar();  // the merged lists are consumed before any warp refills its buffer
-    sp = S.sp;
-    if (VERIFY) {
-      ring_verify_tail(S, j, kk, K, pword, th, stats_out, accept_out, lane, wid);
-      ring_bar();
-    }
-  }
-  if (wid == 0) spec_store(a.spec, blockIdx.x, sp, lane);
+  if (wid == kRingProducer) ring_produce(a, S, n_chunks, lane);
+  else if (wid >= kRingConsumers)
+    ring_finish<VERIFY>(a, S, wid - kRingConsumers, idx_out, bits_out, proofs, th, stats_out, accept_out, lane);
+  else ring_consume(S, a.K, lane, wid);
 }
 
 // ----------------------------------------------------------------------------- record checks
@@ -2162,8 +2299,14 @@ int smem_attr_once(size_t bytes) {
 // hidden pointer) when the caller leaves the launch shape to the library (ctas_per_sm == 0;
 // > 0 or < 0 selects the one-warp-per-chunk kernels, e.g. beside a co-resident commitment).
 constexpr int kRingMinRounds = 4;  // chunks per ring CTA, at least
-int ring_grid(const uint16_t* hidden, int H, int64_t n_chunks, int ctas_per_sm, cudaStream_t st) {
-  if (ctas_per_sm != 0 || H % 8 != 0 || (reinterpret_cast<uintptr_t>(hidden) & 15u)) return 0;
+constexpr int kRingOptIn = -2;     // ctas_per_sm value that selects the ring kernels
+int ring_grid(const uint16_t* hidden, int H, int64_t n_chunks, int ctas_per_sm, cudaStream_t st, bool verify) {
+  // Opt-in only (DESIGN 5.1b): at configuration 2 the ring select runs 3.02-3.11 ms against
+  // 3.05 ms for the one-warp kernel and the ring verify 3.15 against 3.02 ms, and in the
+  // partitioned pipeline its 2 x 111 KiB of shared memory per SM keeps verify(k-2) off the
+  // SMs select(k) holds (320 vs 340 M tokens/s), so auto (0) keeps the one-warp kernels.
+  (void)verify;
+  if (ctas_per_sm != kRingOptIn || H % 8 != 0 || (reinterpret_cast<uintptr_t>(hidden) & 15u)) return 0;
   const int64_t grid = (int64_t)stream_sms(st) * kRingCtasPerSm;
   return n_chunks >= grid * kRingMinRounds ? (int)grid : 0;
 }
@@ -2251,7 +2394,7 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
                                           reinterpret_cast<unsigned long long*>(ws + L.next), part_cnt);
   SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
             reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
-  if (const int rg = ring_grid(hidden, H, n_chunks, ctas_per_sm, st)) {
+  if (const int rg = ring_grid(hidden, H, n_chunks, ctas_per_sm, st, false)) {
     if (smem_attr_once<ring_stream_kernel<false>>(kRingSmem)) return TL_ECUDA;
     ring_stream_kernel<false><<<rg, kRingThreads, kRingSmem, st>>>(a, idx_out, bits_out, nullptr, tl_thresholds{},
                                                                    nullptr, nullptr);
@@ -2356,7 +2499,7 @@ int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   if (n_chunks > 0) {
     SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
               reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
-    const int rg = ring_grid(hidden, H, n_chunks, ctas_per_sm, st);
+    const int rg = ring_grid(hidden, H, n_chunks, ctas_per_sm, st, true);
     if (rg) {
       if (smem_attr_once<ring_stream_kernel<true>>(kRingSmem)) return TL_ECUDA;
     } else if (smem_attr_once<verify_kernel<false>>(kSelSmem) || smem_attr_once<verify_kernel<true>>(kSelSmem)) {
@@ -2462,9 +2605,26 @@ int tl_partition_destroy(void** streams) {
 
 int32_t tl_stream_sms(void* stream) { return stream_sms(static_cast<cudaStream_t>(stream)); }
 
-int32_t tl_ring_grid(const uint16_t* hidden, int32_t H, int64_t n_chunks, int32_t ctas_per_sm, void* stream) {
+#if TL_RING_STATS
+int tl_ring_lab_trace(unsigned* out) {
+  unsigned z = 0;
+  if (cudaMemcpyFromSymbol(out, g_ring_trace, sizeof(g_ring_trace)) != cudaSuccess) return TL_ECUDA;
+  return cudaMemcpyToSymbol(g_ring_trace_n, &z, 4) == cudaSuccess ? TL_OK : TL_ECUDA;
+}
+int tl_ring_lab_stats(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_ring_stats, sizeof(g_ring_stats)) != cudaSuccess) return TL_ECUDA;
+  if (reset) {
+    static const unsigned long long z[8] = {};
+    if (cudaMemcpyToSymbol(g_ring_stats, z, sizeof(z)) != cudaSuccess) return TL_ECUDA;
+  }
+  return TL_OK;
+}
+#endif
+
+int32_t tl_ring_grid(const uint16_t* hidden, int32_t H, int64_t n_chunks, int32_t ctas_per_sm, int32_t verify,
+                     void* stream) {
   if (H < 1 || n_chunks < 0) return TL_EINVAL;
-  return ring_grid(hidden, H, n_chunks, ctas_per_sm, static_cast<cudaStream_t>(stream));
+  return ring_grid(hidden, H, n_chunks, ctas_per_sm, static_cast<cudaStream_t>(stream), verify != 0);
 }
 
 int tl_exact_chains(const void* hidden, int32_t dtype, const int64_t* row_off, int32_t n_roll, int32_t H, int32_t k,

@@ -21,16 +21,20 @@ pytestmark = pytest.mark.gpu
 N_RANDOM = 48
 
 
-def ring_grid(h, H, n_chunks, ctas=0):
-    return int(_ffi.load().tl_ring_grid(h.data_ptr(), H, n_chunks, ctas, torch.cuda.current_stream().cuda_stream))
+RING = -2   # ctas_per_sm that selects the ring kernels for select and verify
+
+
+def ring_grid(h, H, n_chunks, ctas=RING, verify=1):
+    return int(_ffi.load().tl_ring_grid(h.data_ptr(), H, n_chunks, ctas, verify,
+                                        torch.cuda.current_stream().cuda_stream))
 
 
 def both_ways(h_prv, h_val, offs, H, th=api.Thresholds()):
-    """Prove + verify with the ring kernels (auto) and with the one-warp kernels
-    (ctas_per_sm = -1); returns the two plans' host outputs."""
+    """Prove + verify with the ring kernels (ctas_per_sm = -2) and with the one-warp
+    kernels (-1); returns the two plans' host outputs."""
     eng = api.engine()
     outs = []
-    for ctas in (0, -1):
+    for ctas in (RING, -1):
         plan = eng.plan(offs, H)
         plan.select(h_prv, ctas_per_sm=ctas)
         plan.commit()
@@ -155,9 +159,9 @@ def test_ring_speculation_state_is_only_a_hint(fill):
         spec[:, 1] = 0
         spec[:, 2] = 1
         spec[:, 3] = 0x53504543
-    plan.select(prv.view(torch.int16))
+    plan.select(prv.view(torch.int16), ctas_per_sm=RING)
     plan.commit()
-    plan.verify(val.view(torch.int16))
+    plan.verify(val.view(torch.int16), ctas_per_sm=RING)
     torch.cuda.synchronize()
     ref = eng.plan(offs, H)
     ref.select(prv.view(torch.int16), ctas_per_sm=-1)
@@ -171,10 +175,14 @@ def test_ring_speculation_state_is_only_a_hint(fill):
 def test_ring_is_selected_only_where_it_applies():
     h = torch.empty((64, 1024), dtype=torch.bfloat16, device="cuda")
     sms = int(_ffi.load().tl_stream_sms(None))
-    assert ring_grid(h, 1024, 8 * sms) == 2 * sms
-    assert ring_grid(h, 1024, 8 * sms, ctas=16) == 0      # co-resident pipeline shape
+    g = ring_grid(h, 1024, 8 * sms)
+    assert g > 0 and g % sms == 0
+    assert ring_grid(h, 1024, 8 * sms, verify=0) == g
+    assert ring_grid(h, 1024, 8 * sms, ctas=0, verify=0) == 0   # auto keeps the one-warp kernels
+    assert ring_grid(h, 1024, 8 * sms, ctas=0, verify=1) == 0
+    assert ring_grid(h, 1024, 8 * sms, ctas=16) == 0            # co-resident pipeline shape
     assert ring_grid(h, 1024, 8 * sms, ctas=-1) == 0
-    assert ring_grid(h, 1030, 8 * sms) == 0                # chunks not 16-byte aligned
-    assert ring_grid(h, 1024, 2 * sms) == 0                # too few chunks per CTA
-    hv = h.view(-1)[1:1 + 63 * 1024].view(63, 1024)        # unaligned base pointer
+    assert ring_grid(h, 1030, 8 * sms) == 0                     # chunks not 16-byte aligned
+    assert ring_grid(h, 1024, g) == 0                           # too few chunks per CTA
+    hv = h.view(-1)[1:1 + 63 * 1024].view(63, 1024)             # unaligned base pointer
     assert ring_grid(hv, 1024, 8 * sms) == 0
