@@ -268,6 +268,8 @@ class ToplocEngine:
     def _proof_tensor(self, proofs, n_chunks: int) -> torch.Tensor:
         if isinstance(proofs, ProofBatch):
             proofs = proofs.proofs
+        if isinstance(proofs, np.ndarray):  # (n_chunks, 2 + 2K) uint8, e.g. codec.decode's output
+            proofs = torch.from_numpy(np.ascontiguousarray(proofs, dtype=np.uint8))
         if isinstance(proofs, torch.Tensor):
             t = proofs.to(self.device).contiguous()
         else:  # list (per rollout) of list of bytes / hex str, or flat list
