@@ -18,7 +18,9 @@
  *   - calls are stream-ordered and asynchronous on `stream` (a cudaStream_t,
  *     NULL = legacy default stream); no host synchronisation inside;
  *   - return 0 on success or a negative TL_E* code; tl_strerror() names it;
- *   - the library keeps no mutable global state (safe from many host threads,
+ *   - the library's only device globals are the GF(p) inverse tables (1 MiB, built
+ *     once per device by the first tl_commit and immutable afterwards) and a per-kernel
+ *     "attribute set" flag on the host; no other global state (safe from many host threads,
  *     one stream per thread / device);
  *   - a workspace (tl_workspace_bytes) serves one call at a time: calls that may
  *     run concurrently need their own.  Between calls it carries the select
@@ -112,10 +114,12 @@ int tl_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_
 /*
  * Launch-shape variants for pipelining a stream of batches (the commitment of
  * batch k on a second stream, beside verify of batch k-1 and select of k+1).
- * ctas_per_sm = 0 (or -1) runs the one-warp-per-chunk kernels at full occupancy
- * (18 CTAs per SM); > 0 caps that grid (16 leaves the registers for one commit CTA);
- * -2 opts in to the TMA-ring kernels for large batches of 16-byte aligned chunks
- * (H % 8 == 0; two 320-thread CTAs per SM, tl_ring_grid), with identical results;
+ * ctas_per_sm = 0 leaves the shape to the library: batches of at most one chunk per
+ * TMA-ring CTA (2 per SM) with 16-byte aligned chunks (H % 8 == 0) stream through the
+ * TMA-ring kernels (tl_ring_grid), larger ones through the one-warp-per-chunk kernels at
+ * full occupancy (18 CTAs per SM); -1 always selects the one-warp kernels, -2 the ring
+ * kernels wherever the chunks are aligned; > 0 caps the one-warp grid (16 leaves the
+ * registers for one commit CTA).  Results are identical;
  * co_resident = 1 runs the commitment with 8 warps (<= 64 registers) and a 64 KiB
  * half inverse table so that CTA fits beside them.  Results are identical.
  */
@@ -126,9 +130,14 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
 int tl_commit_ex(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_t K,
                  uint8_t* proofs_out, void* workspace, size_t workspace_bytes, int32_t co_resident,
                  void* stream);
+/* Build the GF(p) inverse tables on the current device and wait for them (once per
+ * device; later calls return at once).  Optional: tl_commit builds them itself on first
+ * use, but after tl_prepare a small batch's tl_commit is a single kernel launch.  Not
+ * callable during stream capture (it synchronises). */
+int tl_prepare(void);
+
 /* Grid of the TMA-ring kernel for this call shape (verify = 0: tl_select_ex, 1:
- * tl_verify_ex), or 0 when the one-warp-per-chunk kernels serve it (ctas_per_sm != -2,
- * H % 8 != 0, an unaligned hidden pointer, or fewer than 4 chunks per ring CTA). */
+ * tl_verify_ex), or 0 when the one-warp-per-chunk kernels serve it. */
 int32_t tl_ring_grid(const uint16_t* hidden, int32_t H, int64_t n_chunks, int32_t ctas_per_sm, int32_t verify,
                      void* stream);
 int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,

@@ -58,6 +58,7 @@ SYMBOLS = {
     "tl_partition_create": (c_i32, [c_i32, c_vp, c_vp]),
     "tl_partition_destroy": (c_i32, [c_vp]),
     "tl_stream_sms": (c_i32, [c_vp]),
+    "tl_prepare": (c_i32, []),
     "tl_ring_grid": (c_i32, [c_vp, c_i32, c_i64, c_i32, c_i32, c_vp]),
     "tl_record_checks": (c_i32, [c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tl_synth_bf16": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_u64, c_i32, c_vp, c_vp, c_i32, c_u64, c_vp]),

@@ -184,6 +184,8 @@ class ToplocEngine:
         if not 1 <= self.topk <= _ffi.TL_MAX_K:
             raise ValueError(f"topk must be in [1, {_ffi.TL_MAX_K}]")
         self.lib = _ffi.load()
+        with torch.cuda.device(self.device):  # the inverse tables, once per device (tl_prepare)
+            _ffi.check(self.lib.tl_prepare(), "tl_prepare")
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
         self._ws_done: torch.cuda.Event | None = None  # the last call's use of _ws
         self.proof_bytes = 2 + 2 * self.topk
@@ -595,7 +597,11 @@ class DualStreamPipeline(PartitionedPipeline):
         self.main = torch.cuda.Stream(eng.device)     # select
         self.vstream = torch.cuda.Stream(eng.device)  # verify
         self.side = torch.cuda.Stream(eng.device)     # commit
-        self.co_resident = True
+        # a batch of at most one chunk per SM sub-partition leaves most SMs free: its
+        # commitment runs the 4-warp full-table kernel (one launch once the tables are
+        # prepared) instead of the co-resident form
+        n_chunks = self.plans[0].n_chunks
+        self.co_resident = n_chunks > 4 * int(eng.lib.tl_stream_sms(None))
         self.sms = None
 
 

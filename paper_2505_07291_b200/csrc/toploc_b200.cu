@@ -306,6 +306,8 @@ struct SelArgs {
   int split = 1;                            // warps per chunk (small batches, sel_plan)
   unsigned long long* part = nullptr;       // workspace: [n_chunks][split][K] partial top-k keys
   unsigned* part_cnt = nullptr;             // workspace: per-chunk arrivals (zeroed by chunk_prefix_kernel)
+  int64_t* prefix_out = nullptr;            // ring kernels, small batches: prefix == nullptr, the kernel
+                                            // builds it in shared memory and CTA 0 stores it here
 };
 // Chunk scheduling: the first round is static (chunk = global warp id), later chunks
 // are claimed from a workspace counter, so warps that stream faster (SMs with fewer
@@ -760,12 +762,24 @@ prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restri
 // products, one Fermat inverse per run, back-substitution -- costs ~3 multiplications
 // per entry instead of a ~24-multiplication power each (10.5 us -> a few us per call,
 // which matters for small batches).
+//
+// The tables are a pure function of the primes, so they live in module memory, built once
+// per device: the first tl_commit's inv_table_kernel builds them and its last CTA raises
+// g_inv_ready; every later call only resets the commitment's chunk counter and returns
+// (~1 us instead of 4-6 us on the latency-bound small batches).  Concurrent first calls on
+// several streams each build identical values.
 constexpr int kInvRun = 16;
 constexpr int kInvTableThreads = 256;
 constexpr int kInvTableBlocks = 65536 / (kInvRun * kInvTableThreads);  // per table
-__global__ void inv_table_kernel(uint16_t* __restrict__ tables, unsigned long long* __restrict__ next) {
+constexpr unsigned kInvReady = 0x494E5654u;
+__device__ __align__(128) uint16_t g_inv_tables[kInvTables * 65536];
+__device__ unsigned g_inv_ready;
+__device__ unsigned g_inv_done;
+__global__ void inv_table_kernel(unsigned long long* __restrict__ next) {
   const int q = blockIdx.y;
   if (next && blockIdx.x == 0 && q == 0 && threadIdx.x == 0) *next = 0;  // commit_kernel's chunk counter
+  if (*reinterpret_cast<volatile unsigned*>(&g_inv_ready) == kInvReady) return;
+  uint16_t* tables = g_inv_tables;
   const uint32_t p = kPrimesDesc[q];
   const ModP m(p);
   const uint32_t a0 = (blockIdx.x * blockDim.x + threadIdx.x) * kInvRun;
@@ -793,6 +807,14 @@ __global__ void inv_table_kernel(uint16_t* __restrict__ tables, unsigned long lo
   uint4* dst = reinterpret_cast<uint4*>(tables + (size_t)q * 65536u + a0);
 #pragma unroll
   for (int v = 0; v < kInvRun / 8; ++v) dst[v] = make_uint4(out[4 * v], out[4 * v + 1], out[4 * v + 2], out[4 * v + 3]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&g_inv_done, 1u) == kInvTableBlocks * kInvTables - 1) {
+      __threadfence();
+      atomicExch(&g_inv_ready, kInvReady);
+    }
+  }
 }
 
 // Inverse source for the divided differences: the CTA's shared-memory table (first
@@ -1003,8 +1025,8 @@ __device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32
 template <int WARPS, bool HALF>
 __global__ void __launch_bounds__(WARPS * 32, HALF ? 1024 / (WARPS * 32) : 1)
 commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits, int64_t n_chunks,
-              int K, const uint16_t* __restrict__ inv_tables, uint8_t* __restrict__ proofs,
-              unsigned long long* __restrict__ next) {
+              int K, uint8_t* __restrict__ proofs, unsigned long long* __restrict__ next) {
+  const uint16_t* inv_tables = g_inv_tables;
   constexpr int kTabEntries = HALF ? kHalfTab : 65536;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint16_t* inv0 = reinterpret_cast<uint16_t*>(smem_raw);
@@ -1032,8 +1054,9 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
   const int PB = 2 + 2 * K;
   const int64_t nw = (int64_t)gridDim.x * WARPS;
   // first round static, then chunks claimed from the counter (reset by inv_table_kernel)
+  // (next == nullptr: the grid covers the batch, one chunk per warp, no counter)
   for (int64_t j = (int64_t)blockIdx.x * WARPS + warp; j < n_chunks;) {
-    const unsigned long long claim = lane == 0 ? atomicAdd(next, 1ull) : 0ull;
+    const unsigned long long claim = next && lane == 0 ? atomicAdd(next, 1ull) : (unsigned long long)n_chunks;
     uint32_t raw[4], yb[4];
     int kk = 0;
 #pragma unroll
@@ -1323,6 +1346,7 @@ static_assert(kRingSub * kRingStride * kRingTileU == kRingStageVec && kRingTileU
 constexpr int kRingCap = TL_MAX_K + 32;  // per-warp candidate keys: a compaction keeps kk, one round adds <= 32
 constexpr int kRingCtasPerSm = TL_RING_CTAS;
 
+constexpr int kRingOwnPrefixMax = 256;  // rollouts whose chunk prefix a small-batch ring CTA builds itself
 struct RingMeta {
   long long j;               // chunk (-1: no more work)
   unsigned long long theta;  // the chunk's starting threshold (stamped on every stage)
@@ -1346,6 +1370,7 @@ struct RingSmem {
   RingJob job[2];
   int cnt[2][kRingConsumers];  // candidates per consumer warp at the chunk end
   int cmp[2][kRingConsumers];  // ... and whether its threshold was raised by a compaction
+  int64_t pfx[kRingOwnPrefixMax + 1];  // small batches: the chunk prefix, built by the CTA itself
   unsigned long long theta_next;  // speculation for the next chunk (finishers -> producer)
   Spec spec;                      // the CTA's speculation state, updated in chunk order ...
   long long spec_seq;             // ... by the finisher of chunk spec_seq
@@ -1512,7 +1537,10 @@ __device__ __forceinline__ void ring_produce(const SelArgs& a, RingSmem& S, int6
       }
       return;
     }
-    const unsigned long long claim = lane == 0 ? atomicAdd(a.next, 1ull) : 0ull;  // the next chunk
+    // the next chunk (none to claim when the grid covers the batch: small batches run without
+    // the counter reset of chunk_prefix_kernel)
+    const unsigned long long claim = lane == 0 && (int64_t)gridDim.x < n_chunks ? atomicAdd(a.next, 1ull)
+                                                                                 : (unsigned long long)n_chunks;
     const int bytes = 2 * g.n;
     const int nst = (bytes + kRingStageBytes - 1) / kRingStageBytes;
     if (lane == 0) {
@@ -1772,6 +1800,33 @@ ring_stream_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restric
     S.spec = spec_load(a.spec, blockIdx.x);
     S.spec_seq = 0;
     S.theta_next = S.spec.theta;
+  }
+  if (a.prefix == nullptr) {
+    // small batch (<= kRingOwnPrefixMax rollouts): this CTA builds the chunk prefix itself,
+    // sparing the chunk_prefix_kernel launch; CTA 0 leaves a copy for rollout_verdict_kernel
+    for (int r = threadIdx.x; r < a.n_roll; r += blockDim.x) {
+      const int64_t T = a.row_off[r + 1] - a.row_off[r];
+      S.pfx[r + 1] = T > 0 ? (T + a.C - 1) / a.C : 0;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      int64_t carry = 0;
+      for (int base = 0; base < a.n_roll; base += 32) {
+        int64_t v = base + lane < a.n_roll ? S.pfx[base + lane + 1] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int64_t y = __shfl_up_sync(0xFFFFFFFFu, v, o);
+          if (lane >= o) v += y;
+        }
+        if (base + lane < a.n_roll) S.pfx[base + lane + 1] = carry + v;
+        carry += __shfl_sync(0xFFFFFFFFu, v, 31);
+      }
+      if (lane == 0) S.pfx[0] = 0;
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && a.prefix_out)
+      for (int r = threadIdx.x; r <= a.n_roll; r += blockDim.x) a.prefix_out[r] = S.pfx[r];
+    a.prefix = S.pfx;
   }
   __syncthreads();
   const int64_t n_chunks = min(a.n_chunks, a.prefix[a.n_roll]);
@@ -2147,7 +2202,7 @@ __global__ void synth_kernel(uint16_t* __restrict__ out, int64_t row0, int64_t n
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t spec, next, prefix, tables, idx, bits, accept, part, part_cnt, total;
+  size_t spec, next, prefix, idx, bits, accept, part, part_cnt, total;
 };
 WsLayout ws_layout(int32_t n_roll, int64_t n_chunks, int32_t K) {
   WsLayout L;
@@ -2155,7 +2210,6 @@ WsLayout ws_layout(int32_t n_roll, int64_t n_chunks, int32_t K) {
   L.spec = o; o += (size_t)kSpecSlots * 16;  // first, so its offset never depends on the shape
   L.next = o; o += 256;                       // chunk counters: [0] streaming kernels, [1] commit
   L.prefix = o; o = align_up(o + (size_t)(n_roll + 1) * 8, 256);
-  L.tables = o; o = align_up(o + (size_t)kInvTables * 65536 * 2, 256);
   L.idx = o; o = align_up(o + (size_t)n_chunks * K * 4, 256);
   L.bits = o; o = align_up(o + (size_t)n_chunks * K * 2, 256);
   L.accept = o; o = align_up(o + (size_t)n_chunks, 256);
@@ -2300,25 +2354,37 @@ int smem_attr_once(size_t bytes) {
 // > 0 or < 0 selects the one-warp-per-chunk kernels, e.g. beside a co-resident commitment).
 constexpr int kRingMinRounds = 4;  // chunks per ring CTA, at least
 constexpr int kRingOptIn = -2;     // ctas_per_sm value that selects the ring kernels
+// A ring launch whose grid covers the batch (no chunk claims) over at most
+// kRingOwnPrefixMax rollouts builds its chunk prefix itself (no chunk_prefix_kernel).
+bool ring_own_prefix(int rg, int64_t n_chunks, int n_roll) {
+  return rg > 0 && n_chunks <= rg && n_roll <= kRingOwnPrefixMax;
+}
+
 int ring_grid(const uint16_t* hidden, int H, int64_t n_chunks, int ctas_per_sm, cudaStream_t st, bool verify) {
-  // Opt-in only (DESIGN 5.1b): at configuration 2 the ring select runs 3.02-3.11 ms against
-  // 3.05 ms for the one-warp kernel and the ring verify 3.15 against 3.02 ms, and in the
-  // partitioned pipeline its 2 x 111 KiB of shared memory per SM keeps verify(k-2) off the
-  // SMs select(k) holds (320 vs 340 M tokens/s), so auto (0) keeps the one-warp kernels.
+  // Auto (0) takes the ring only for batches of at most one chunk per ring CTA, where a
+  // chunk streamed by a whole CTA (all its stages in flight at once) finishes sooner than
+  // by two warps of the split kernels: configuration 1 select 26 vs 34 us, 1 x 8192 x 5120
+  // 39 vs 48 us.  Larger batches keep the one-warp kernels (DESIGN 5.1b: at configuration 2
+  // the ring select runs 3.02-3.11 ms against 3.05 ms and the ring verify 3.15 against 3.02
+  // ms, and in the partitioned pipeline its 2 x 111 KiB of shared memory per SM keeps
+  // verify(k-2) off the SMs select(k) holds).  -2 opts in at any size.
   (void)verify;
-  if (ctas_per_sm != kRingOptIn || H % 8 != 0 || (reinterpret_cast<uintptr_t>(hidden) & 15u)) return 0;
+  if ((ctas_per_sm != kRingOptIn && ctas_per_sm != 0) || H % 8 != 0 ||
+      (reinterpret_cast<uintptr_t>(hidden) & 15u))
+    return 0;
   const int64_t grid = (int64_t)stream_sms(st) * kRingCtasPerSm;
-  return n_chunks >= grid * kRingMinRounds ? (int)grid : 0;
+  if (ctas_per_sm == 0 && n_chunks > grid) return 0;
+  return (int)min(grid, max(n_chunks, (int64_t)1));
 }
 
 template <int WARPS, bool HALF>
-int launch_commit_t(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, const uint16_t* tables,
-                    uint8_t* proofs, unsigned long long* next, cudaStream_t st) {
+int launch_commit_t(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, uint8_t* proofs,
+                    unsigned long long* next, cudaStream_t st) {
   const size_t smem = (size_t)(HALF ? kHalfTab : 65536) * 2 + (2 * 128 + kHashSlots) * WARPS * 4;
   if (smem_attr_once<commit_kernel<WARPS, HALF>>(smem)) return TL_ECUDA;
   int grid = stream_sms(st);  // one CTA per SM of the stream's partition
   if ((int64_t)grid * WARPS > n_chunks) grid = (int)((n_chunks + WARPS - 1) / WARPS);
-  commit_kernel<WARPS, HALF><<<grid, WARPS * 32, smem, st>>>(idx, bits, n_chunks, K, tables, proofs, next);
+  commit_kernel<WARPS, HALF><<<grid, WARPS * 32, smem, st>>>(idx, bits, n_chunks, K, proofs, next);
   return launch_status();
 }
 
@@ -2328,12 +2394,19 @@ int launch_commit_t(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, 
 // chunk's warp then has a sub-partition to itself and the call is one chunk's latency
 // (a 32-warp CTA would stack 8 chunks on each sub-partition of a few SMs).
 constexpr int kSmallCommitWarps = 4;
-int launch_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, const uint16_t* tables,
-                  uint8_t* proofs, unsigned long long* next, int co_resident, cudaStream_t st) {
-  if (co_resident) return launch_commit_t<kCoCommitWarps, true>(idx, bits, n_chunks, K, tables, proofs, next, st);
+// Devices whose inverse tables are known built and visible to every stream (tl_prepare).
+std::atomic<uint32_t> g_tables_prepared{0u};
+bool tables_prepared() {
+  int dev = 0;
+  return cudaGetDevice(&dev) == cudaSuccess && (g_tables_prepared.load(std::memory_order_acquire) >> (dev & 31)) & 1u;
+}
+
+int launch_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, uint8_t* proofs,
+                  unsigned long long* next, int co_resident, cudaStream_t st) {
+  if (co_resident) return launch_commit_t<kCoCommitWarps, true>(idx, bits, n_chunks, K, proofs, next, st);
   if (n_chunks <= (int64_t)stream_sms(st) * kSmallCommitWarps)
-    return launch_commit_t<kSmallCommitWarps, false>(idx, bits, n_chunks, K, tables, proofs, next, st);
-  return launch_commit_t<kCommitWarps, false>(idx, bits, n_chunks, K, tables, proofs, next, st);
+    return launch_commit_t<kSmallCommitWarps, false>(idx, bits, n_chunks, K, proofs, next, st);
+  return launch_commit_t<kCommitWarps, false>(idx, bits, n_chunks, K, proofs, next, st);
 }
 
 }  // namespace
@@ -2390,11 +2463,17 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   int64_t* prefix = reinterpret_cast<int64_t*>(ws + L.prefix);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   unsigned* part_cnt = reinterpret_cast<unsigned*>(ws + L.part_cnt);
-  chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix,
-                                          reinterpret_cast<unsigned long long*>(ws + L.next), part_cnt);
   SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
             reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
-  if (const int rg = ring_grid(hidden, H, n_chunks, ctas_per_sm, st, false)) {
+  const int rg = ring_grid(hidden, H, n_chunks, ctas_per_sm, st, false);
+  if (ring_own_prefix(rg, n_chunks, n_roll)) {
+    a.prefix = nullptr;  // built in the ring kernel
+    a.prefix_out = prefix;
+  } else {
+    chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix,
+                                            reinterpret_cast<unsigned long long*>(ws + L.next), part_cnt);
+  }
+  if (rg) {
     if (smem_attr_once<ring_stream_kernel<false>>(kRingSmem)) return TL_ECUDA;
     ring_stream_kernel<false><<<rg, kRingThreads, kRingSmem, st>>>(a, idx_out, bits_out, nullptr, tl_thresholds{},
                                                                    nullptr, nullptr);
@@ -2440,14 +2519,16 @@ int tl_commit_ex(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int
   if (n_chunks == 0) return TL_OK;
   if (!idx || !bits || !proofs_out || !workspace) return TL_EINVAL;
   const WsLayout L = ws_layout(0, n_chunks, K);
-  if (workspace_bytes < L.tables + (size_t)kInvTables * 65536 * 2 || (reinterpret_cast<uintptr_t>(workspace) & 255))
-    return TL_EWORKSPACE;
+  if (workspace_bytes < L.next + 256 || (reinterpret_cast<uintptr_t>(workspace) & 255)) return TL_EWORKSPACE;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  uint16_t* tables = reinterpret_cast<uint16_t*>(ws + L.tables);
   unsigned long long* next = reinterpret_cast<unsigned long long*>(ws + L.next) + 1;  // commit's own counter
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  inv_table_kernel<<<dim3(kInvTableBlocks, kInvTables), kInvTableThreads, 0, st>>>(tables, next);
-  return launch_commit(idx, bits, n_chunks, K, tables, proofs_out, next, co_resident, st);
+  // a small batch (one chunk per warp of the 4-warp grid) on a device whose tables are
+  // prepared is one launch: no table build, no chunk counter
+  if (!co_resident && n_chunks <= (int64_t)stream_sms(st) * kSmallCommitWarps && tables_prepared())
+    return launch_commit(idx, bits, n_chunks, K, proofs_out, nullptr, 0, st);
+  inv_table_kernel<<<dim3(kInvTableBlocks, kInvTables), kInvTableThreads, 0, st>>>(next);
+  return launch_commit(idx, bits, n_chunks, K, proofs_out, next, co_resident, st);
 }
 
 int tl_prove(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll, int64_t n_rows,
@@ -2494,12 +2575,18 @@ int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
   unsigned* part_cnt = reinterpret_cast<unsigned*>(ws + L.part_cnt);
-  chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix,
-                                          reinterpret_cast<unsigned long long*>(ws + L.next), part_cnt);
+  const int rg = n_chunks > 0 ? ring_grid(hidden, H, n_chunks, ctas_per_sm, st, true) : 0;
+  const bool own_prefix = ring_own_prefix(rg, n_chunks, n_roll);
+  if (!own_prefix)
+    chunk_prefix_kernel<<<1, 1024, 0, st>>>(row_off, n_roll, C, prefix,
+                                            reinterpret_cast<unsigned long long*>(ws + L.next), part_cnt);
   if (n_chunks > 0) {
     SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
               reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
-    const int rg = ring_grid(hidden, H, n_chunks, ctas_per_sm, st, true);
+    if (own_prefix) {
+      a.prefix = nullptr;  // built in the ring kernel
+      a.prefix_out = prefix;
+    }
     if (rg) {
       if (smem_attr_once<ring_stream_kernel<true>>(kRingSmem)) return TL_ECUDA;
     } else if (smem_attr_once<verify_kernel<false>>(kSelSmem) || smem_attr_once<verify_kernel<true>>(kSelSmem)) {
@@ -2604,6 +2691,20 @@ int tl_partition_destroy(void** streams) {
 }
 
 int32_t tl_stream_sms(void* stream) { return stream_sms(static_cast<cudaStream_t>(stream)); }
+
+int tl_prepare(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TL_ECUDA;
+  if ((g_tables_prepared.load(std::memory_order_acquire) >> (dev & 31)) & 1u) return TL_OK;
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return TL_ECUDA;
+  inv_table_kernel<<<dim3(kInvTableBlocks, kInvTables), kInvTableThreads, 0, st>>>(nullptr);
+  const bool ok = cudaGetLastError() == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess;
+  cudaStreamDestroy(st);
+  if (!ok) return TL_ECUDA;
+  g_tables_prepared.fetch_or(1u << (dev & 31), std::memory_order_acq_rel);
+  return TL_OK;
+}
 
 #if TL_RING_STATS
 int tl_ring_lab_trace(unsigned* out) {

@@ -70,7 +70,9 @@ def check_case(prv, val, offs, H, th=api.Thresholds(), n_random=N_RANDOM):
     return ring
 
 
-@pytest.mark.parametrize("R,T,H", [(40, 1024, 5120),      # 10 stages per chunk
+@pytest.mark.parametrize("R,T,H", [(1, 2048, 1024),       # configuration 1: auto picks the ring
+                                   (1, 8192, 5120), (3, 700, 5120), (2, 33, 8192),
+                                   (40, 1024, 5120),      # 10 stages per chunk
                                    (64, 1024, 1024),      # 2 stages
                                    (48, 1024, 8192),      # 16 stages
                                    (10, 8192, 128)])      # a chunk is a quarter of one stage
@@ -178,11 +180,12 @@ def test_ring_is_selected_only_where_it_applies():
     g = ring_grid(h, 1024, 8 * sms)
     assert g > 0 and g % sms == 0
     assert ring_grid(h, 1024, 8 * sms, verify=0) == g
-    assert ring_grid(h, 1024, 8 * sms, ctas=0, verify=0) == 0   # auto keeps the one-warp kernels
+    assert ring_grid(h, 1024, 8 * sms, ctas=0, verify=0) == 0   # auto: large batches keep the one-warp kernels
     assert ring_grid(h, 1024, 8 * sms, ctas=0, verify=1) == 0
+    assert ring_grid(h, 1024, 64, ctas=0, verify=1) == 64       # auto: a batch of one chunk per ring CTA
+    assert ring_grid(h, 1024, g, ctas=0) == g and ring_grid(h, 1024, g + 1, ctas=0) == 0
     assert ring_grid(h, 1024, 8 * sms, ctas=16) == 0            # co-resident pipeline shape
-    assert ring_grid(h, 1024, 8 * sms, ctas=-1) == 0
-    assert ring_grid(h, 1030, 8 * sms) == 0                     # chunks not 16-byte aligned
-    assert ring_grid(h, 1024, g) == 0                           # too few chunks per CTA
+    assert ring_grid(h, 1024, 64, ctas=-1) == 0
+    assert ring_grid(h, 1030, 64, ctas=0) == 0                  # chunks not 16-byte aligned
     hv = h.view(-1)[1:1 + 63 * 1024].view(63, 1024)             # unaligned base pointer
-    assert ring_grid(hv, 1024, 8 * sms) == 0
+    assert ring_grid(hv, 1024, 64, ctas=0) == 0
