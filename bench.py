@@ -780,6 +780,9 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if rank == 0:  # the communicator the verdict gather uses (NCCL's own INIT lines need NCCL_DEBUG=INFO)
+            print(f"bench: NCCL communicator up: nranks {world} (NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}, "
+                  f"one process per GPU)", file=sys.stderr, flush=True)
     try:
         run_b200(args, cfg, rank, world, local_rank)
     finally:
