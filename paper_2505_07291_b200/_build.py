@@ -57,5 +57,18 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     return lib
 
 
+CHECKED_LIB = os.path.join(OUT_DIR, "libtoploc_b200_checked.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """The -DTL_CHECKED=1 library: device asserts on the index, workspace and chunk-geometry
+    arithmetic (tests/test_gpu_checked.py runs the GPU fuzz suites against it; select it with
+    TOPLOC_B200_LIB)."""
+    if not force and os.path.exists(CHECKED_LIB) and os.path.getmtime(CHECKED_LIB) >= max(
+            os.path.getmtime(f) for f in _deps()):
+        return CHECKED_LIB
+    return build(force=True, out=CHECKED_LIB, defines=("TL_CHECKED=1",))
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

@@ -21,6 +21,7 @@
 #include <cuda_fp16.h>
 #include <stddef.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include <atomic>
 
@@ -81,6 +82,28 @@ constexpr int kCoCommitWarps = TL_CO_COMMIT_WARPS;
 constexpr int kNddUnroll = TL_NDD_UNROLL;
 constexpr int kConvUnroll = TL_CONV_UNROLL;
 constexpr uint32_t kPMax = 65497u;
+
+// ----------------------------------------------------------------------------- checked builds
+// -DTL_CHECKED=1 (paper_2505_07291_b200/_build.py: build_checked) compiles device asserts on
+// the index, workspace and chunk-geometry arithmetic: a violated bound prints where and
+// traps (the launch fails with an error instead of reading or writing out of bounds).  The
+// GPU fuzz and parity tests run once more against that library (tests/test_gpu_checked.py);
+// compute-sanitizer is not available on the GPU pool, so this is its substitute.
+#ifndef TL_CHECKED
+#define TL_CHECKED 0
+#endif
+#if TL_CHECKED
+#define TL_CHECK(cond)                                                                              \
+  do {                                                                                              \
+    if (!(cond)) {                                                                                  \
+      printf("TL_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x, #cond);                                                              \
+      __trap();                                                                                     \
+    }                                                                                               \
+  } while (0)
+#else
+#define TL_CHECK(cond) do {} while (0)
+#endif
 
 // ----------------------------------------------------------------------------- helpers
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
@@ -306,6 +329,7 @@ struct SelArgs {
   int split = 1;                            // warps per chunk (small batches, sel_plan)
   unsigned long long* part = nullptr;       // workspace: [n_chunks][split][K] partial top-k keys
   unsigned* part_cnt = nullptr;             // workspace: per-chunk arrivals (zeroed by chunk_prefix_kernel)
+  int64_t n_rows = 0;                       // rows of hidden (bounds checks of -DTL_CHECKED builds)
   int64_t* prefix_out = nullptr;            // ring kernels, small batches: prefix == nullptr, the kernel
                                             // builds it in shared memory and CTA 0 stores it here
 };
@@ -320,6 +344,8 @@ __device__ __forceinline__ unsigned long long claim_chunk(const SelArgs& a, int 
 
 __device__ __forceinline__ ChunkGeo chunk_geo(const SelArgs& a, int64_t j) {
   const ChunkRef cr = locate_chunk(a.prefix, a.row_off, a.n_roll, j, a.C);
+  TL_CHECK(j >= 0 && cr.rollout >= 0 && cr.rollout < a.n_roll && cr.rows >= 1 && cr.rows <= a.C);
+  TL_CHECK(cr.row_start >= 0 && cr.row_start + cr.rows <= a.n_rows);
   ChunkGeo g;
   g.base = a.hidden + cr.row_start * (int64_t)a.H;
   g.n = cr.rows * a.H;
@@ -429,6 +455,7 @@ __device__ __forceinline__ void warp_append(bool p, unsigned long long key, unsi
     p = p && key >= theta;
     bal = __ballot_sync(0xFFFFFFFFu, p);
   }
+  TL_CHECK(cnt + __popc(bal) <= kWarpCap);
   if (p) wb[cnt + __popc(bal & lanemask_lt())] = key;
   cnt += __popc(bal);
   __syncwarp();
@@ -512,6 +539,7 @@ __device__ __forceinline__ void pass_warp(const ChunkGeo& cg, WarpScan& w, int k
         hm |= ((gbase + u * 32 < nvec && coarse_hit(mu[u], c2)) ? 1u : 0u) << u;
       if (hm) {
         int pos = atomicAdd(w.lst_n, __popc(hm));
+        TL_CHECK(pos + __popc(hm) <= kStageVec);
 #pragma unroll
         for (int u = 0; u < kSelU; ++u) {
           if ((hm >> u) & 1u) {
@@ -636,6 +664,7 @@ __device__ __forceinline__ bool select_split(const SelArgs& a, const ChunkGeo& g
   const int hi = s == S - 1 ? g.n : (int)(((int64_t)g.n * (s + 1) / S) & ~7ll);
   const int kks = min(K, hi - lo);
   if (kks > 0) select_chunk(sub_geo(g, lo, hi), kks, slot, sp, lane PROF_PASS);
+  TL_CHECK(j < kSplitMaxChunks && (j * S + s + 1) * K <= (int64_t)kSplitMaxLists * TL_MAX_K && lo <= hi && hi <= g.n);
   unsigned long long* mine = a.part + ((size_t)j * S + s) * K;
   for (int i = lane; i < K; i += 32) mine[i] = i < kks ? slot.wbuf[i] - ((unsigned long long)lo << 16) : 0ull;
   __threadfence();
@@ -738,9 +767,11 @@ prove_select_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restri
     } else {
       select_chunk(g, kk, slot, sp, lane PROF_PASS);
     }
+    TL_CHECK(j < n_chunks && kk <= K && K <= TL_MAX_K);
     for (int i = lane; i < K; i += 32) {
       if (i < kk) {
         const unsigned long long v = slot.wbuf[i];
+        TL_CHECK(key_idx(v) < (unsigned)g.n);
         idx_out[j * K + i] = (int32_t)key_idx(v);
         bits_out[j * K + i] = (uint16_t)(v & 0xFFFFu);
       } else {
@@ -1069,6 +1100,7 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
       yb[r] = b;
       kk += __popc(__ballot_sync(0xFFFFFFFFu, iv >= 0));
     }
+    TL_CHECK(j < n_chunks && kk <= K && K <= TL_MAX_K);
     // a small-batch CTA (one chunk per sub-partition) is latency-bound: unroll deeper so the
     // inverse lookups of later levels are issued ahead of the divided-difference chain
     commit_chunk<HALF ? kInvSmemHalf : kInvSmem, WARPS <= 4 ? 8 : kNddUnroll, WARPS <= 4 ? 4 : kConvUnroll>(
@@ -1089,6 +1121,7 @@ __device__ __forceinline__ void verify_tail_warp(const unsigned long long* top, 
                                                  uint16_t* coef, const tl_thresholds& th,
                                                  tl_chunk_stats* __restrict__ stats_out, uint8_t* __restrict__ accept_out,
                                                  int64_t j, int lane) {
+  TL_CHECK(j >= 0 && kk >= 1 && kk <= K && K <= TL_MAX_K);
   // claimed coefficients (big-endian u16) -> coef, zero-padded to TL_MAX_K
   unsigned p = 0;
 #pragma unroll
@@ -1267,6 +1300,7 @@ __global__ void rollout_verdict_kernel(const uint8_t* __restrict__ chunk_accept,
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= n_roll) return;
+  TL_CHECK(prefix[r] >= 0 && prefix[r] <= prefix[r + 1]);
   int ok = 1;
   for (int64_t q = prefix[r] + lane; q < prefix[r + 1]; q += 32) ok &= (q < n_chunks && chunk_accept[q]) ? 1 : 0;
   ok = __all_sync(0xFFFFFFFFu, ok);
@@ -1406,6 +1440,7 @@ __device__ __forceinline__ void ring_append(bool p, unsigned long long key, Ring
     p = p && key >= w.theta;
     bal = __ballot_sync(0xFFFFFFFFu, p);
   }
+  TL_CHECK(w.cnt + __popc(bal) <= kRingCap);
   if (p) w.wb[w.cnt + __popc(bal & lanemask_lt())] = key;
   w.cnt += __popc(bal);
   __syncwarp();
@@ -1501,6 +1536,7 @@ __device__ __forceinline__ ChunkGeo warp_chunk_geo(const SelArgs& a, int64_t j, 
   }
   const int64_t r0 = a.row_off[lo], T = a.row_off[lo + 1] - r0;
   const int64_t local = j - a.prefix[lo];
+  TL_CHECK(lo < a.n_roll && local >= 0 && local * a.C < T && r0 + local * a.C + min((int64_t)a.C, T - local * a.C) <= a.n_rows);
   ChunkGeo g;
   g.base = a.hidden + (r0 + local * a.C) * (int64_t)a.H;
   g.n = (int)min((int64_t)a.C, T - local * a.C) * a.H;
@@ -1521,6 +1557,8 @@ __device__ __forceinline__ void ring_produce(const SelArgs& a, RingSmem& S, int6
     const int s = (int)(t % kRingStages);
     if (t >= kRingStages) mbar_wait_parity(&S.empty[s], (unsigned)(((t / kRingStages) - 1) & 1));
     const int len = min(kRingStageBytes, bytes - q * kRingStageBytes);
+    TL_CHECK(j >= 0 && j < n_chunks && len > 0 && (len & 15) == 0 && q < nst && g.n <= a.C * a.H);
+    TL_CHECK((reinterpret_cast<uintptr_t>(g.base) & 15u) == 0);
     S.meta[s] = RingMeta{(long long)j, theta, q, nst, len, g.n};
     mbar_expect_tx(&S.full[s], (uint32_t)len);
     bulk_copy_g2s(S.ring[s], reinterpret_cast<const uint8_t*>(g.base) + (size_t)q * kRingStageBytes, (uint32_t)len,
@@ -1648,6 +1686,7 @@ __device__ __forceinline__ void ring_finish(const SelArgs& a, RingSmem& S, int f
     unsigned long long acc[4];
     int retry = 0;
     bool released = false;
+    TL_CHECK(j >= 0 && kk >= 1 && kk <= K && total >= 0);
     if (total >= kk && total <= kWarpCap) {
       // the usual case: gather the consumers' candidates (slot p of the concatenation is
       // key p - pre[w] of warp w) and rank the union once
@@ -1666,6 +1705,7 @@ __device__ __forceinline__ void ring_finish(const SelArgs& a, RingSmem& S, int f
 #pragma unroll
         for (int q = 1; q < kRingConsumers; ++q) w += __shfl_sync(0xFFFFFFFFu, pre, q) <= pos ? 1 : 0;
         const int off = pos - __shfl_sync(0xFFFFFFFFu, pre, w);
+        TL_CHECK(pos >= total || (w < kRingConsumers && off >= 0 && off < S.cnt[b][w]));
         if (pos < total) uni[pos] = S.wbuf[b][w][off];
       }
       __syncwarp();
@@ -2465,6 +2505,7 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   unsigned* part_cnt = reinterpret_cast<unsigned*>(ws + L.part_cnt);
   SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
             reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
+  a.n_rows = n_rows;
   const int rg = ring_grid(hidden, H, n_chunks, ctas_per_sm, st, false);
   if (ring_own_prefix(rg, n_chunks, n_roll)) {
     a.prefix = nullptr;  // built in the ring kernel
@@ -2583,6 +2624,7 @@ int tl_verify_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
   if (n_chunks > 0) {
     SelArgs a{hidden, row_off, prefix, reinterpret_cast<uint4*>(ws + L.spec),
               reinterpret_cast<unsigned long long*>(ws + L.next), n_roll, H, C, K, n_chunks};
+    a.n_rows = n_rows;
     if (own_prefix) {
       a.prefix = nullptr;  // built in the ring kernel
       a.prefix_out = prefix;
