@@ -76,9 +76,9 @@ PRIME_SET = frozenset(PRIMES_DESC)
 class Thresholds:
     """Verdict thresholds (explicit parameters; defaults documented in DESIGN.md)."""
 
-    max_exp_mismatch: int = 38      # >= 90 of 128 exponents must agree
-    max_mant_mean: float = 10.0
-    max_mant_median: float = 8.0
+    max_exp_mismatch: int = 28      # measured defaults, as api.Thresholds (profiles/r02_calibration.json)
+    max_mant_mean: float = 7.0
+    max_mant_median: float = 5.0
 
 
 @dataclass
