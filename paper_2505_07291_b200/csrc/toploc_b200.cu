@@ -38,6 +38,18 @@ constexpr int kSelThreads = TL_SEL_THREADS;   // select CTA threads (independent
 #ifndef TL_SEL_U
 #define TL_SEL_U 8
 #endif
+// L2 bulk prefetch in the one-warp streaming loop: lane 0 issues one
+// cp.async.bulk.prefetch.L2 of TL_L2_PREFETCH_TILES warp tiles (4 KiB each) every that many
+// tiles, TL_L2_PREFETCH_AHEAD tiles ahead of the register double buffer's loads.  Measured at
+// configuration 2 (tools/stream_probe.py, same process): select 3.057 -> 3.005-3.015 ms,
+// verify ~1.5 % faster; more than ~32 KiB ahead per warp (2664 warps) thrashes the 126 MB
+// L2 (8 tiles at 16 ahead: 5.1 ms).  0 disables it.
+#ifndef TL_L2_PREFETCH_TILES
+#define TL_L2_PREFETCH_TILES 4
+#endif
+#ifndef TL_L2_PREFETCH_AHEAD
+#define TL_L2_PREFETCH_AHEAD 2
+#endif
 constexpr int kSelU = TL_SEL_U;               // 16-B vectors per lane per warp tile
 #ifndef TL_SEL_MIN_BLOCKS
 #define TL_SEL_MIN_BLOCKS 18
@@ -513,8 +525,25 @@ __device__ __forceinline__ void pass_warp(const ChunkGeo& cg, WarpScan& w, int k
     const int g = lane + u * 32;
     vn[u] = g < nvec ? ld_stream(vb + g) : make_uint4(0u, 0u, 0u, 0u);
   }
+#if TL_L2_PREFETCH_TILES
+  // bulk L2 prefetch of the chunk's first TL_L2_PREFETCH_AHEAD tiles, then a group of
+  // TL_L2_PREFETCH_TILES tiles that far ahead every TL_L2_PREFETCH_TILES tiles (lane 0)
+  if (lane == 0) {
+    const int v0 = 0, v1 = min(nvec, (TL_L2_PREFETCH_AHEAD) * kWTileVec);
+    if (v1 > v0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vb + v0), "r"((unsigned)(v1 - v0) * 16u) : "memory");
+  }
+#endif
   for (int it = 0; it < cg.nst; ++it) {
     const int gbase = it * kWTileVec + lane;
+#if TL_L2_PREFETCH_TILES
+    if (lane == 0 && it % TL_L2_PREFETCH_TILES == 0) {
+      const int v0 = (it + TL_L2_PREFETCH_AHEAD) * kWTileVec;
+      const int v1 = min(nvec, v0 + TL_L2_PREFETCH_TILES * kWTileVec);
+      if (v1 > v0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vb + v0), "r"((unsigned)(v1 - v0) * 16u) : "memory");
+    }
+#endif
     uint4 v[kSelU];
 #pragma unroll
     for (int u = 0; u < kSelU; ++u) {
