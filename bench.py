@@ -45,6 +45,18 @@ AUTO_PIPELINE_MIN_CHUNKS = 2048
 LAUNCHES_PER_STEP = 7      # select: prefix+select; commit: inv_table+commit; verify: prefix+verify+verdict
 
 
+def launches_per_step(eng, hidden, plan, co_resident: bool) -> int:
+    """Kernels one prove+verify step launches: 7 for large batches; a batch the ring grid
+    covers (<= 256 rollouts) needs no chunk_prefix_kernel (select 1, verify 2), and a small
+    commitment on a prepared device is one launch (DESIGN 5.1b, 5.2)."""
+    import torch
+    st = torch.cuda.current_stream(hidden.device).cuda_stream
+    g = int(eng.lib.tl_ring_grid(hidden.data_ptr(), plan.H, plan.n_chunks, 0, 0, st))
+    own_prefix = 0 < plan.n_chunks <= g and plan.n_roll <= 256
+    small_commit = not co_resident and plan.n_chunks <= 4 * int(eng.lib.tl_stream_sms(st))
+    return (1 if own_prefix else 2) + (1 if small_commit else 2) + (2 if own_prefix else 3)
+
+
 def algorithmic_bytes_per_token(H: int) -> float:
     """prove reads 2H + writes 258/32; verify reads 2H + 258/32."""
     return 4 * H + 2 * PROOF_BYTES / CHUNK
@@ -688,7 +700,7 @@ def run_b200(args, cfg, rank, world, local_rank):
             "cpu_baseline": cpu,
             "exact_mode": exact,
             "e2e": e2e,
-            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "gpu_launches": launches_per_step(eng, prv, plan, args.schedule == "pipeline") * args.steps,
             "comm": ({"backend": "nccl", "nranks": world, "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
                       "data_path_collectives": 0, "collective": "one all_gather of the per-rollout verdict bytes"}
                      if world > 1 else None),
