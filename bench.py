@@ -286,6 +286,25 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def e2e_rollouts(args, R, T, H, dev) -> int:
+    """Rollouts per GPU in the e2e leg: --e2e-rollouts, or (0, the default) the whole batch
+    when its pinned host copies (prover + validator) fit in 40 % of the host's available
+    memory shared by this node's ranks and its device copies in 80 % of the free HBM; else
+    as many as fit, at least 16."""
+    if args.e2e_rollouts > 0:
+        return min(R, args.e2e_rollouts)
+    import torch
+    per = 2 * T * H * 2
+    local = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+    try:
+        import psutil
+        host = psutil.virtual_memory().available * 0.4 / local
+    except Exception:
+        host = 16 * per
+    dev_free = torch.cuda.mem_get_info(dev)[0] * 0.8
+    return int(max(min(R, 16), min(R, host // per, dev_free // per)))
+
+
 # ----------------------------------------------------------------------------- host placement
 _AFFINITY0 = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
 
@@ -582,13 +601,14 @@ def run_b200(args, cfg, rank, world, local_rank):
     # e2e through the public API with host buffers (bounded sample of rollouts)
     e2e = None
     if args.e2e:
-        Re = min(R, args.e2e_rollouts)
+        Re = e2e_rollouts(args, R, T, H, dev)
         rows = Re * T
         numa = pin_to_gpu_numa_node(dev)   # pinned buffers first-touched on the GPU's NUMA node
         hp = torch.empty((rows, H), dtype=torch.bfloat16, pin_memory=True)
         hv = torch.empty((rows, H), dtype=torch.bfloat16, pin_memory=True)
-        hp.copy_(prv[:rows].cpu())
-        hv.copy_(val[:rows].cpu())
+        hp.copy_(prv[:rows])
+        hv.copy_(val[:rows])
+        torch.cuda.synchronize(dev)
         offs_e = offs[:Re + 1]
         times = []
         h2d = d2h = 0
@@ -609,11 +629,12 @@ def run_b200(args, cfg, rank, world, local_rank):
                 times.append(a.elapsed_time(b))
             h2d = 2 * rows * H * 2 + proofs_host.numel() + (len(offs_e)) * 8 * 2
             d2h = proofs_host.numel() + verdict_host.numel()
+        del hp, hv  # the pinned copies (whole batch: 43 GB) before the CPU legs
         te = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": world * rows / (float(te.item()) / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "rollouts_per_gpu": Re,
+               "d2h_bytes_per_step": d2h, "rollouts_per_gpu": Re, "of_rollouts_per_gpu": R,
                "h2d_gbs_per_gpu": h2d / (float(te.item()) / 1e3) / 1e9, "host_numa": numa,
                "note": "public API (ToplocEngine.prove/verify) from pinned host tensors; proofs and verdicts read "
                        "back; bound by the host link (h2d_gbs_per_gpu against ~55 GB/s for PCIe 5 x16)"}
@@ -736,7 +757,9 @@ def main():
     ap.add_argument("--dist", default="normal", choices=["normal", "massive"])
     ap.add_argument("--rollouts", type=int, default=0, help="override the configuration's rollout count (sweeps)")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
-    ap.add_argument("--e2e-rollouts", type=int, default=16)
+    ap.add_argument("--e2e-rollouts", type=int, default=0,
+                    help="rollouts per GPU through the public API from host memory (0: the whole batch when "
+                         "host and device memory allow, e2e_rollouts())")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-exact", dest="exact", action="store_false",
