@@ -834,7 +834,7 @@ constexpr int kInvTableBlocks = 65536 / (kInvRun * kInvTableThreads);  // per ta
 constexpr unsigned kInvReady = 0x494E5654u;
 __device__ __align__(128) uint16_t g_inv_tables[kInvTables * 65536];
 __device__ unsigned g_inv_ready;
-__device__ unsigned g_inv_done;
+__device__ unsigned g_inv_pieces[(kInvTableBlocks * kInvTables + 31) / 32];  // written pieces, one bit each
 __global__ void inv_table_kernel(unsigned long long* __restrict__ next) {
   const int q = blockIdx.y;
   if (next && blockIdx.x == 0 && q == 0 && threadIdx.x == 0) *next = 0;  // commit_kernel's chunk counter
@@ -869,11 +869,21 @@ __global__ void inv_table_kernel(unsigned long long* __restrict__ next) {
   for (int v = 0; v < kInvRun / 8; ++v) dst[v] = make_uint4(out[4 * v], out[4 * v + 1], out[4 * v + 2], out[4 * v + 3]);
   __syncthreads();
   if (threadIdx.x == 0) {
+    // mark this piece written; the CTA that completes the set raises the flag.  Per-piece
+    // bits (not a count) keep concurrent first launches on several streams safe: the flag
+    // never rises before every piece was written by some launch.
     __threadfence();
-    if (atomicAdd(&g_inv_done, 1u) == kInvTableBlocks * kInvTables - 1) {
-      __threadfence();
-      atomicExch(&g_inv_ready, kInvReady);
+    constexpr int kWords = (kInvTableBlocks * kInvTables + 31) / 32;
+    const int piece = q * kInvTableBlocks + blockIdx.x;
+    atomicOr(&g_inv_pieces[piece >> 5], 1u << (piece & 31));
+    __threadfence();
+    bool all = true;
+    for (int w = 0; w < kWords; ++w) {
+      const int bits_in = min(32, kInvTableBlocks * kInvTables - 32 * w);
+      const unsigned want = bits_in == 32 ? 0xFFFFFFFFu : (1u << bits_in) - 1u;
+      all = all && (atomicOr(&g_inv_pieces[w], 0u) & want) == want;
     }
+    if (all) atomicExch(&g_inv_ready, kInvReady);
   }
 }
 

@@ -694,3 +694,44 @@ def test_pipeline_graph_matches_serial():
     torch.cuda.synchronize()
     assert got[0].tolist() == [0, 0, 0]
     pipe.close()
+
+
+def test_first_commits_on_two_streams_without_prepare_build_correct_tables():
+    """The inverse tables are built by the first tl_commit when tl_prepare was not called.
+    Two first calls racing on two streams of a fresh process must both produce the oracle's
+    proofs (the ready flag rises only when every table piece was written)."""
+    import subprocess
+    import sys
+    code = r'''
+import ctypes, numpy as np, torch
+from oracle import toploc_oracle as TO
+from oracle.synth_cpu import synth_bits
+from paper_2505_07291_b200 import _ffi
+L = _ffi.load()                       # no ToplocEngine: tl_prepare is never called
+H, T = 2048, 256
+offs = np.array([0, T], dtype=np.int64)
+outs = []
+streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+bits = [synth_bits(0, T, H, seed=s, dist=1) for s in (1, 2)]
+for s, b in zip(streams, bits):
+    h = torch.from_numpy(b.view(np.int16)).cuda()
+    od = torch.from_numpy(offs).cuda()
+    n = T // 32
+    ws = torch.empty(int(L.tl_workspace_bytes(1, n, 128)), dtype=torch.uint8, device="cuda")
+    pr = torch.empty((n, 258), dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    outs.append((h, od, ws, pr, s, b))
+for h, od, ws, pr, s, b in outs:      # both launched back to back, no sync between them
+    rc = L.tl_prove(h.data_ptr(), od.data_ptr(), 1, T, H, 32, 128, T // 32, pr.data_ptr(), None, None,
+                    ws.data_ptr(), ws.numel(), s.cuda_stream)
+    assert rc == 0
+torch.cuda.synchronize()
+for h, od, ws, pr, s, b in outs:
+    want = TO.build_proofs(b, offs)[0]
+    got = [bytes(r) for r in pr.cpu().numpy()]
+    assert got == want
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
