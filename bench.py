@@ -198,6 +198,7 @@ class CpuPool:
         for _ in range(warmup):
             self.step()
         res = [self.step() for _ in range(steps)]
+        self.step_ms = [round(r[0] * 1e3, 1) for r in res]
         wall = sum(r[0] for r in res)
         return sum(r[1] for r in res) / wall, wall / len(res), all(r[2] for r in res)
 
@@ -249,7 +250,7 @@ def cpu_baseline_block(cfg, steps: int, warmup: int, exact_steps: int = 1):
         pool.close()
     what = "whole" if T == cfg["T"] else f"{T}-token slices of"
     out = {"value": tps, "unit": "tokens/s", "cores": workers, "kind": "port", "per_core": tps / workers,
-           "ms_per_step": per_step * 1e3, "steps": steps, "all_accepted": ok,
+           "ms_per_step": per_step * 1e3, "steps": steps, "all_accepted": ok, "step_ms": pool.step_ms,
            "sample": f"per step {workers} processes (one per host core) each prove+verify {what} {cfg['T']}-token "
                      f"rollout(s) x H={H} with oracle/toploc_oracle.py; data and the port's inverse tables built "
                      f"before timing"}
