@@ -167,15 +167,10 @@ struct ModP {
 };
 
 // True iff p is one of the moduli a prover can emit: a prime in [32771, 65497]
-// (kPrimesDesc).  Warp-uniform binary search over the descending table.
+// (kPrimesDesc), by one load from the generated membership map (a binary search of the
+// constant table cost ~12 dependent constant-cache misses on a latency-bound chunk tail).
 __device__ __forceinline__ bool prover_prime(uint32_t p) {
-  if (p < kPrimesDesc[TL_N_PRIMES - 1] || p > kPrimesDesc[0]) return false;
-  int lo = 0, hi = TL_N_PRIMES - 1;  // kPrimesDesc[lo] >= p >= kPrimesDesc[hi]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (kPrimesDesc[mid] >= p) lo = mid; else hi = mid;
-  }
-  return kPrimesDesc[lo] == p || kPrimesDesc[hi] == p;
+  return p < 65536u && ((__ldg(&kProverModulusBits[p >> 5]) >> (p & 31)) & 1u);
 }
 
 // Chunk j -> (rollout, first row, rows) by binary search over the chunk prefix.
@@ -1156,11 +1151,23 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
 // statistics and verdict.  coef (TL_MAX_K u16, 16-B aligned) is the warp's shared
 // scratch.
 constexpr int kPW = (TL_MAX_K + 1 + 31) / 32;  // proof words per lane
+#if TL_RING_STATS
+__device__ unsigned long long g_vt[8];  // lab: verify-tail phase cycles (decode, Horner, compare, median, write)
+#endif
+// PS: evaluate by Paterson-Stockmeyer (shorter chains, ~40 registers more; the ring
+// finisher) instead of the two-half Horner (the one-warp kernel, 18 CTAs per SM).
+template <bool PS>
 __device__ __forceinline__ void verify_tail_warp(const unsigned long long* top, int kk, int K, const uint32_t (&pword)[kPW],
                                                  uint16_t* coef, const tl_thresholds& th,
                                                  tl_chunk_stats* __restrict__ stats_out, uint8_t* __restrict__ accept_out,
                                                  int64_t j, int lane) {
   TL_CHECK(j >= 0 && kk >= 1 && kk <= K && K <= TL_MAX_K);
+#if TL_RING_STATS
+  long long vt_ = clock64();
+#define VT_MARK(i) do { const long long t_ = clock64(); if (lane == 0) atomicAdd(&g_vt[i], (unsigned long long)(t_ - vt_)); vt_ = t_; } while (0)
+#else
+#define VT_MARK(i) do {} while (0)
+#endif
   // claimed coefficients (big-endian u16) -> coef, zero-padded to TL_MAX_K
   unsigned p = 0;
 #pragma unroll
@@ -1175,6 +1182,7 @@ __device__ __forceinline__ void verify_tail_warp(const unsigned long long* top, 
   // a proof is only as strong as its modulus: anything but one of the prover's primes
   // (p = 2 with zero coefficients would match every exponent) is a bad proof
   const bool bad = !prover_prime(p);
+  VT_MARK(0);
   unsigned mism = 0, msum = 0, nmatch = 0;
   uint32_t dv[4] = {0xFFu, 0xFFu, 0xFFu, 0xFFu};  // |mantissa diff| of each exponent-equal point, else 0xFF
   if (!bad) {
@@ -1186,34 +1194,74 @@ __device__ __forceinline__ void verify_tail_warp(const unsigned long long* top, 
       x[r] = i < kk ? m.red(key_idx(top[i])) : 0u;
       acc[r] = 0u;
     }
-    // P(x) = L(x) + x^64 U(x) over the zero-padded TL_MAX_K coefficients: eight independent
-    // 64-step Horner chains per lane instead of four 128-step ones (half the latency)
-    static_assert(TL_MAX_K == 128, "two 64-coefficient halves");
+    static_assert(TL_MAX_K == 128, "two 64-coefficient halves / 16 blocks of 8 coefficients");
     const uint4* c8 = reinterpret_cast<const uint4*>(coef);
-    uint32_t hi[4];
+    if (!PS) {
+      // P(x) = L(x) + x^64 U(x): eight independent 64-step Horner chains per lane instead of
+      // four 128-step ones (half the latency; the one-warp kernel's registers allow no more)
+      uint32_t hi[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) hi[r] = 0u;
+      for (int r = 0; r < 4; ++r) hi[r] = 0u;
 #pragma unroll 1
-    for (int kb = 7; kb >= 0; --kb) {
-      const uint4 ql = c8[kb], qh = c8[kb + 8];
-      const uint32_t cl[4] = {ql.x, ql.y, ql.z, ql.w}, ch[4] = {qh.x, qh.y, qh.z, qh.w};
+      for (int kb = 7; kb >= 0; --kb) {
+        const uint4 ql = c8[kb], qh = c8[kb + 8];
+        const uint32_t cl[4] = {ql.x, ql.y, ql.z, ql.w}, ch[4] = {qh.x, qh.y, qh.z, qh.w};
 #pragma unroll
-      for (int e = 7; e >= 0; --e) {
-        const uint32_t a_ = (cl[e >> 1] >> (16 * (e & 1))) & 0xFFFFu, b_ = (ch[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+        for (int e = 7; e >= 0; --e) {
+          const uint32_t a_ = (cl[e >> 1] >> (16 * (e & 1))) & 0xFFFFu, b_ = (ch[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
 #pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            acc[r] = m.red(acc[r] * x[r] + a_);
+            hi[r] = m.red(hi[r] * x[r] + b_);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        uint32_t x64 = x[r];
+#pragma unroll
+        for (int s = 0; s < 6; ++s) x64 = m.mul(x64, x64);
+        acc[r] = m.add(acc[r], m.mul(x64, hi[r]));
+      }
+    } else {
+      // Paterson-Stockmeyer over the zero-padded TL_MAX_K coefficients:
+      //   P(x) = sum_k y^k Q_k(x),  y = x^8,  Q_k(x) = sum_{i<8} c_{8k+i} x^i.
+      // Each Q_k is eight independent 32x32->64 multiply-adds of (raw u16 coefficient) x
+      // (x^i mod p) -- below 2^35, reduced once -- and only the 16 steps in y form a
+      // dependent chain: ~40 % fewer instructions than Horner over 128 coefficients and a
+      // quarter of its chain (the same residue: any evaluation order of P mod p).
+      const uint32_t k32 = (uint32_t)(0x100000000ull % m.p);  // 2^32 mod p
+      uint32_t xp[4][8], y[4];
+  #pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        xp[r][0] = 1u;
+        xp[r][1] = x[r];
+        xp[r][2] = m.mul(x[r], x[r]);
+        xp[r][3] = m.mul(xp[r][2], x[r]);
+        xp[r][4] = m.mul(xp[r][2], xp[r][2]);
+        xp[r][5] = m.mul(xp[r][4], x[r]);
+        xp[r][6] = m.mul(xp[r][4], xp[r][2]);
+        xp[r][7] = m.mul(xp[r][4], xp[r][3]);
+        y[r] = m.mul(xp[r][4], xp[r][4]);
+      }
+  #pragma unroll 2
+      for (int kb = 15; kb >= 0; --kb) {
+        const uint4 q = c8[kb];
+        const uint32_t cw[4] = {q.x, q.y, q.z, q.w};
+        uint32_t cc[8];
+  #pragma unroll
+        for (int e = 0; e < 8; ++e) cc[e] = (cw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+  #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          acc[r] = m.red(acc[r] * x[r] + a_);
-          hi[r] = m.red(hi[r] * x[r] + b_);
+          unsigned long long s = 0ull;
+  #pragma unroll
+          for (int e = 0; e < 8; ++e) s += (unsigned long long)cc[e] * xp[r][e];
+          const uint32_t qk = m.red(m.red((uint32_t)s) + (uint32_t)(s >> 32) * k32);  // s < 2^35
+          acc[r] = m.red(acc[r] * y[r] + qk);
         }
       }
     }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      uint32_t x64 = x[r];
-#pragma unroll
-      for (int s = 0; s < 6; ++s) x64 = m.mul(x64, x64);
-      acc[r] = m.add(acc[r], m.mul(x64, hi[r]));
-    }
+    VT_MARK(1);
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int i = lane + 32 * r;
@@ -1231,6 +1279,7 @@ __device__ __forceinline__ void verify_tail_warp(const unsigned long long* top, 
       }
     }
   }
+  VT_MARK(2);
   mism = __reduce_add_sync(0xFFFFFFFFu, mism);
   msum = __reduce_add_sync(0xFFFFFFFFu, msum);
   const unsigned nm = __reduce_add_sync(0xFFFFFFFFu, nmatch);
@@ -1253,6 +1302,7 @@ __device__ __forceinline__ void verify_tail_warp(const unsigned long long* top, 
   };
   const unsigned q1 = nm ? (nm - 1) / 2 : 0, q2 = nm / 2;
   const int v1 = (int)select_rank(q1), v2 = q2 == q1 ? v1 : (int)select_rank(q2);
+  VT_MARK(3);
   if (lane == 0) {
     tl_chunk_stats st;
     if (bad) {
@@ -1277,6 +1327,8 @@ __device__ __forceinline__ void verify_tail_warp(const unsigned long long* top, 
     accept_out[j] = (uint8_t)(st.flags & TL_STAT_ACCEPT);
   }
   __syncwarp();
+  VT_MARK(4);
+#undef VT_MARK
 }
 
 // Verify: the warp selects its chunk's top-kk on the validator tensor, evaluates
@@ -1320,7 +1372,7 @@ verify_kernel(SelArgs a, const uint8_t* __restrict__ proofs, tl_thresholds th,
       select_chunk(g, kk, slot, sp, lane PROF_PASS);
     }
 
-    verify_tail_warp(slot.wbuf, kk, K, pword, slot.coef, th, stats_out, accept_out, j, lane);
+    verify_tail_warp<false>(slot.wbuf, kk, K, pword, slot.coef, th, stats_out, accept_out, j, lane);
     __syncwarp();
     PROF_MARK(4);
     if (SPLIT) break;  // one part per warp
@@ -1587,7 +1639,8 @@ __device__ __forceinline__ ChunkGeo warp_chunk_geo(const SelArgs& a, int64_t j, 
 
 // Producer warp: lane 0 issues the stages; the whole warp locates the next chunk while the
 // current one streams (the ring is full then, so the producer would only be waiting).
-__device__ __forceinline__ void ring_produce(const SelArgs& a, RingSmem& S, int64_t n_chunks, int lane) {
+__device__ __forceinline__ void ring_produce(const SelArgs& a, RingSmem& S, int64_t n_chunks, int lane,
+                                             const uint8_t* __restrict__ proofs = nullptr) {
   int64_t j = blockIdx.x;
   ChunkGeo g = warp_chunk_geo(a, j < n_chunks ? j : 0, lane);
   long long t = 0;
@@ -1624,6 +1677,8 @@ __device__ __forceinline__ void ring_produce(const SelArgs& a, RingSmem& S, int6
       theta = *reinterpret_cast<volatile unsigned long long*>(&S.theta_next);  // the finishers' latest hint
       issue(0, nst, bytes);
     }
+    if (proofs && lane < 3)  // verify: the chunk's 258-byte proof into L2 for its finisher
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(proofs + j * (2 + 2 * a.K) + 128 * lane));
     __syncwarp();
     const int64_t jn = (int64_t)gridDim.x + (int64_t)__shfl_sync(0xFFFFFFFFu, claim, 0);
     const ChunkGeo gn = warp_chunk_geo(a, jn < n_chunks ? jn : 0, lane);
@@ -1800,7 +1855,12 @@ __device__ __forceinline__ void ring_finish(const SelArgs& a, RingSmem& S, int f
     }
     // speculation, one CTA-wide state updated in chunk order by the two finishers (theta
     // only rises by a compaction: a chunk with too many candidates)
-    const unsigned long long kth = __shfl_sync(0xFFFFFFFFu, acc[(kk - 1) >> 5], (kk - 1) & 31);
+#if TL_RING_STATS
+    const long long t_merged = clock64();
+#endif
+    const int kr = (kk - 1) >> 5;  // register of the kk-th key (a select chain: no local-memory array)
+    const unsigned long long kreg = kr == 0 ? acc[0] : kr == 1 ? acc[1] : kr == 2 ? acc[2] : acc[3];
+    const unsigned long long kth = __shfl_sync(0xFFFFFFFFu, kreg, (kk - 1) & 31);
     while (*reinterpret_cast<volatile long long*>(&S.spec_seq) != cseq) __nanosleep(64);  // leave the issue slots to the scans
     Spec sp = S.spec;
     int d = sp.delta;
@@ -1823,7 +1883,17 @@ __device__ __forceinline__ void ring_finish(const SelArgs& a, RingSmem& S, int f
 #pragma unroll
       for (int r = 0; r < 4; ++r) S.uni[f][32 * r + lane] = acc[r];
       __syncwarp();
-      verify_tail_warp(S.uni[f], kk, K, pword, S.coef[f], th, stats_out, accept_out, j, lane);
+#if TL_RING_STATS
+      const long long t_spec = clock64();
+#endif
+      verify_tail_warp<true>(S.uni[f], kk, K, pword, S.coef[f], th, stats_out, accept_out, j, lane);
+#if TL_RING_STATS
+      if (lane == 0) {
+        atomicAdd(&g_ring_stats[5], (unsigned long long)(t_merged - t0));
+        atomicAdd(&g_ring_stats[6], (unsigned long long)(t_spec - t_merged));
+        atomicAdd(&g_ring_stats[7], (unsigned long long)(clock64() - t_spec));
+      }
+#endif
     } else {
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
@@ -1909,7 +1979,7 @@ ring_stream_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restric
   }
   __syncthreads();
   const int64_t n_chunks = min(a.n_chunks, a.prefix[a.n_roll]);
-  if (wid == kRingProducer) ring_produce(a, S, n_chunks, lane);
+  if (wid == kRingProducer) ring_produce(a, S, n_chunks, lane, VERIFY ? proofs : nullptr);
   else if (wid >= kRingConsumers)
     ring_finish<VERIFY>(a, S, wid - kRingConsumers, idx_out, bits_out, proofs, th, stats_out, accept_out, lane);
   else ring_consume(S, a.K, lane, wid);
@@ -2788,6 +2858,11 @@ int tl_prepare(void) {
 }
 
 #if TL_RING_STATS
+int tl_ring_lab_vt(unsigned long long* out) {
+  static const unsigned long long z[8] = {};
+  if (cudaMemcpyFromSymbol(out, g_vt, sizeof(g_vt)) != cudaSuccess) return TL_ECUDA;
+  return cudaMemcpyToSymbol(g_vt, z, sizeof(z)) == cudaSuccess ? TL_OK : TL_ECUDA;
+}
 int tl_ring_lab_trace(unsigned* out) {
   unsigned z = 0;
   if (cudaMemcpyFromSymbol(out, g_ring_trace, sizeof(g_ring_trace)) != cudaSuccess) return TL_ECUDA;

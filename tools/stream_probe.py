@@ -67,13 +67,19 @@ def main():
             out["ring_stats_select"] = {"chunks": buf[0], "candidates_per_chunk": buf[1] / n,
                                         "rescans_per_chunk": buf[2] / n, "compacting_warps_per_chunk": buf[3] / n,
                                         "tail_us_per_chunk": buf[4] / n / 1.9e3}
+            vt = (ctypes.c_ulonglong * 8)()
+            eng.lib.tl_ring_lab_vt(vt)
             plan.verify(val, ctas_per_sm=ctas)
             torch.cuda.synchronize()
             lab(buf, 1)
+            eng.lib.tl_ring_lab_vt(vt)
+            out["verify_tail_phase_us"] = [round(vt[i] / max(1, buf[0]) / 1.9e3, 3) for i in range(5)]
             n = max(1, buf[0])
             out["ring_stats_verify"] = {"chunks": buf[0], "candidates_per_chunk": buf[1] / n,
                                         "rescans_per_chunk": buf[2] / n, "compacting_warps_per_chunk": buf[3] / n,
-                                        "tail_us_per_chunk": buf[4] / n / 1.9e3}
+                                        "tail_us_per_chunk": buf[4] / n / 1.9e3,
+                                        "merge_us": buf[5] / n / 1.9e3, "spec_us": buf[6] / n / 1.9e3,
+                                        "verify_tail_us": buf[7] / n / 1.9e3}
         gb = R * T * H * 2 / 1e9
         out[mode] = {"select_ms": min(sel), "select_gbs": gb / min(sel) * 1e3,
                      "commit_verify_ms": min(ver)}
