@@ -30,7 +30,9 @@
  * Layout
  *   hidden   : bf16 bit patterns, row-major (n_rows, H), rollouts concatenated
  *              along rows; row_off[n_roll + 1] (int64) delimits rollout r as rows
- *              [row_off[r], row_off[r+1]).
+ *              [row_off[r], row_off[r+1]): non-decreasing, row_off[0] >= 0 and
+ *              row_off[n_roll] <= n_rows (device memory, so not validated on the host;
+ *              the -DTL_CHECKED build traps on a chunk outside [0, n_rows)).
  *   chunk j  : the j-th block of C rows of a rollout (final block partial),
  *              numbered across rollouts in order; n_chunks = sum ceil(T_r / C).
  *   proofs   : uint8 [n_chunks][2 + 2K]  (K = 128 -> 258 bytes) :
