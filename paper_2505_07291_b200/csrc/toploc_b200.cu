@@ -1497,6 +1497,7 @@ struct RingSmem {
   int cmp[2][kRingConsumers];  // ... and whether its threshold was raised by a compaction
   int64_t pfx[kRingOwnPrefixMax + 1];  // small batches: the chunk prefix, built by the CTA itself
   unsigned long long theta_next;  // speculation for the next chunk (finishers -> producer)
+  unsigned long long theta_pub[2];  // by chunk parity: the largest threshold a consumer's compaction proved
   Spec spec;                      // the CTA's speculation state, updated in chunk order ...
   long long spec_seq;             // ... by the finisher of chunk spec_seq
 };
@@ -1507,6 +1508,7 @@ struct RingScan {
   unsigned long long theta;
   int cnt;
   unsigned long long* wb;
+  unsigned long long* pub = nullptr;  // the chunk's shared threshold (consumers; nullptr on a re-scan)
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -1528,6 +1530,9 @@ __device__ __forceinline__ void ring_append(bool p, unsigned long long key, Ring
   if (w.cnt + __popc(bal) > kRingCap) {
     w.theta = ring_compact(w.wb, w.cnt, kk, lane);
     w.cnt = kk;
+    // this warp now holds kk keys >= theta, so no element below it is in the chunk's top-kk:
+    // the other consumer warps adopt it (ties in a heavy-tie chunk stop queueing everywhere)
+    if (w.pub && lane == 0) atomicMax(w.pub, w.theta);
     p = p && key >= w.theta;
     bal = __ballot_sync(0xFFFFFFFFu, p);
   }
@@ -1561,6 +1566,11 @@ __device__ __forceinline__ void ring_scan(const uint4* __restrict__ src, int nve
     for (int u = 0; u < kRingTileU; ++u) {
       const int g = g0 + u * kRingStride;
       v[u] = g < nvec ? (SMEM ? src[g] : ld_stream(src + g)) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    if (SMEM && w.pub) {  // adopt a threshold another warp's compaction published
+      unsigned long long tp = lane == 0 ? *reinterpret_cast<volatile unsigned long long*>(w.pub) : 0ull;
+      tp = __shfl_sync(0xFFFFFFFFu, tp, 0);
+      if (tp > w.theta) w.theta = tp;
     }
     const unsigned c2 = coarse_c2(w.theta, elem0 + 8u * (unsigned)(g0 - lane));
     unsigned mu[kRingTileU];
@@ -1710,6 +1720,7 @@ __device__ __forceinline__ void ring_consume(RingSmem& S, int K, int lane, int w
       const int b = (int)(c & 1);
       if (c >= 2 && TL_RING_LAB != 2) mbar_wait_parity(&S.freed[b], (unsigned)(((c >> 1) - 1) & 1));  // c - 2 merged
       w.wb = S.wbuf[b][wid];
+      w.pub = &S.theta_pub[b];
       theta0 = TL_RING_LAB == 2 ? (0x4050ull << 40) : m.theta;  // lab build 2: a fixed typical threshold, no finish
       w.theta = theta0;
       w.cnt = 0;
@@ -1781,31 +1792,34 @@ __device__ __forceinline__ void ring_finish(const SelArgs& a, RingSmem& S, int f
     int retry = 0;
     bool released = false;
     TL_CHECK(j >= 0 && kk >= 1 && kk <= K && total >= 0);
-    if (total >= kk && total <= kWarpCap) {
-      // the usual case: gather the consumers' candidates (slot p of the concatenation is
-      // key p - pre[w] of warp w) and rank the union once
-      int cw = lane < kRingConsumers ? S.cnt[b][lane] : 0, pre = cw;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xFFFFFFFFu, pre, o);
-        if (lane >= o) pre += y;
-      }
-      pre -= cw;  // exclusive prefix of the warps' counts, lane w
+    // gather the consumers' candidates at or above the chunk's shared threshold (a key below
+    // it has kk keys above it in the warp that proved it) into the union scratch
+    const unsigned long long theta_f = S.theta_pub[b];
+    int kept = 0;
+    if (total >= kk) {
       unsigned long long* uni = S.uni[f];
-#pragma unroll
-      for (int r = 0; r < kWarpCap / 32; ++r) {
-        const int pos = 32 * r + lane;
-        int w = 0;
-#pragma unroll
-        for (int q = 1; q < kRingConsumers; ++q) w += __shfl_sync(0xFFFFFFFFu, pre, q) <= pos ? 1 : 0;
-        const int off = pos - __shfl_sync(0xFFFFFFFFu, pre, w);
-        TL_CHECK(pos >= total || (w < kRingConsumers && off >= 0 && off < S.cnt[b][w]));
-        if (pos < total) uni[pos] = S.wbuf[b][w][off];
+#pragma unroll 1
+      for (int q = 0; q < kRingConsumers; ++q) {
+        const int cq = S.cnt[b][q];
+        for (int i0 = 0; i0 < cq; i0 += 32) {
+          const unsigned long long key = i0 + lane < cq ? S.wbuf[b][q][i0 + lane] : 0ull;
+          const bool keep = i0 + lane < cq && key >= theta_f;
+          const unsigned bal = __ballot_sync(0xFFFFFFFFu, keep);
+          const int pos = kept + __popc(bal & lanemask_lt());
+          if (keep && pos < kWarpCap) uni[pos] = key;
+          kept += __popc(bal);
+        }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.freed[b]);  // the consumers may refill their buffers already
+    }
+    if (total >= kk && kept <= kWarpCap) {
+      unsigned long long* uni = S.uni[f];
+      if (lane == 0) {
+        S.theta_pub[b] = 0ull;
+        mbar_arrive(&S.freed[b]);  // the consumers may refill their buffers already
+      }
       released = true;
-      final_sort<kWarpCap / 32, TL_MAX_K>(uni, total, lane);
+      final_sort<kWarpCap / 32, TL_MAX_K>(uni, kept, lane);
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc[r] = uni[32 * r + lane];
     } else if (total >= kk) {
@@ -1923,7 +1937,10 @@ __device__ __forceinline__ void ring_finish(const SelArgs& a, RingSmem& S, int f
     }
 #endif
     __syncwarp();
-    if (lane == 0 && !released) mbar_arrive(&S.freed[b]);
+    if (lane == 0 && !released) {
+      S.theta_pub[b] = 0ull;
+      mbar_arrive(&S.freed[b]);
+    }
   }
   if (f == 0) spec_store(a.spec, blockIdx.x, S.spec, lane);
 }
@@ -1948,6 +1965,7 @@ ring_stream_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restric
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     S.spec = spec_load(a.spec, blockIdx.x);
     S.spec_seq = 0;
+    S.theta_pub[0] = S.theta_pub[1] = 0ull;
     S.theta_next = S.spec.theta;
   }
   if (a.prefix == nullptr) {
