@@ -684,7 +684,7 @@ def run_b200(args, cfg, rank, world, local_rank):
     cpu = None
     if args.cpu_baseline and rank == 0:   # after the timed region; the other ranks wait at the final barrier
         restore_affinity()
-        cpu = cpu_baseline_block(cfg, steps=3, warmup=1)
+        cpu = cpu_baseline_block(cfg, steps=10, warmup=2)
 
     if rank == 0:
         line = {
