@@ -189,3 +189,19 @@ def test_ring_is_selected_only_where_it_applies():
     assert ring_grid(h, 1030, 64, ctas=0) == 0                  # chunks not 16-byte aligned
     hv = h.view(-1)[1:1 + 63 * 1024].view(63, 1024)             # unaligned base pointer
     assert ring_grid(hv, 1024, 64, ctas=0) == 0
+
+
+def test_ring_small_batch_over_many_tiny_rollouts():
+    """A small batch (one chunk per ring CTA) over more rollouts than a CTA builds its own
+    chunk prefix for (> 256): the chunk_prefix_kernel path with no chunk claims, with empty
+    rollouts in between and partial chunks."""
+    rng = np.random.default_rng(12)
+    T = rng.integers(1, 33, size=300)
+    T[::5] = 0
+    offs = np.concatenate([[0], np.cumsum(T)]).astype(np.int64)
+    n_chunks = int(np.sum(-(-T // 32)))
+    H = 1024
+    prv = synth_device(int(offs[-1]), H, seed=41)
+    assert 256 < len(T) and 0 < n_chunks <= ring_grid(prv, H, n_chunks, ctas=0, verify=0)
+    val = synth_device(int(offs[-1]), H, seed=41, jitter_thr=3277, jitter_seed=42)
+    check_case(prv, val, offs, H)
