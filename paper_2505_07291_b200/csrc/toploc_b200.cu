@@ -311,6 +311,14 @@ __device__ __forceinline__ unsigned hmaxabs2(unsigned a, unsigned b) {
 __device__ __forceinline__ bool coarse_hit(unsigned m, unsigned c2) {
   return (((m & 0x7FFF7FFFu) + c2) & 0x80008000u) != 0u;
 }
+// Coarse-test bits of one 16-B vector's 8 elements (bit e: |element e| >= the tile threshold).
+__device__ __forceinline__ uint32_t elem_mask8(const uint4& v, unsigned c2) {
+  const uint32_t f0 = ((v.x & 0x7FFF7FFFu) + c2) & 0x80008000u, f1 = ((v.y & 0x7FFF7FFFu) + c2) & 0x80008000u;
+  const uint32_t f2 = ((v.z & 0x7FFF7FFFu) + c2) & 0x80008000u, f3 = ((v.w & 0x7FFF7FFFu) + c2) & 0x80008000u;
+  return ((f0 >> 15) & 1u) | ((f0 >> 30) & 2u) | ((f1 >> 13) & 4u) | ((f1 >> 28) & 8u) | ((f2 >> 11) & 16u) |
+         ((f2 >> 26) & 32u) | ((f3 >> 9) & 64u) | ((f3 >> 24) & 128u);
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned r;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
@@ -1542,13 +1550,6 @@ __device__ __forceinline__ void ring_append(bool p, unsigned long long key, Ring
   __syncwarp();
 }
 
-// Coarse-test bits of one 16-B vector's 8 elements (bit e: |element e| >= the tile threshold).
-__device__ __forceinline__ uint32_t elem_mask8(const uint4& v, unsigned c2) {
-  const uint32_t f0 = ((v.x & 0x7FFF7FFFu) + c2) & 0x80008000u, f1 = ((v.y & 0x7FFF7FFFu) + c2) & 0x80008000u;
-  const uint32_t f2 = ((v.z & 0x7FFF7FFFu) + c2) & 0x80008000u, f3 = ((v.w & 0x7FFF7FFFu) + c2) & 0x80008000u;
-  return ((f0 >> 15) & 1u) | ((f0 >> 30) & 2u) | ((f1 >> 13) & 4u) | ((f1 >> 28) & 8u) | ((f2 >> 11) & 16u) |
-         ((f2 >> 26) & 32u) | ((f3 >> 9) & 64u) | ((f3 >> 24) & 128u);
-}
 
 // Share `wid` of one stage-sized piece of the chunk (nvec 16-B vectors at src, in shared
 // memory for the ring or in global memory for a re-scan): vectors
