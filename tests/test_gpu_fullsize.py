@@ -190,3 +190,15 @@ def _zero_first_chunk(prv, R, T, C):
     rows = (torch.arange(R, device=prv.device) * T)[:, None] + torch.arange(C, device=prv.device)[None, :]
     t[rows.reshape(-1)] = 0
     return t
+
+
+def test_configs4_whole_batch_sampled_against_oracle():
+    """configs[4] whole: 1024 rollouts x 4096 tokens, hidden 8192 -- 2 x 68.7 GB in HBM
+    (skipped when the device has less than 150 GB free)."""
+    torch.cuda.empty_cache()
+    if torch.cuda.mem_get_info()[0] < 150e9:
+        pytest.skip("needs 150 GB of free device memory")
+    res, plan = full_check(1024, 4096, 8192)
+    assert plan.n_chunks == 131072 and res["chunks_checked"] >= 512
+    del plan
+    torch.cuda.empty_cache()
