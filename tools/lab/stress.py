@@ -1,0 +1,88 @@
+"""Lab: randomized stress of the streaming kernels -- for random batch shapes, hidden sizes,
+value distributions and validator perturbations, prove + verify through the TMA-ring
+kernels (ctas_per_sm -2), the one-warp kernels (-1) and the library's choice (0), compare
+every output over the whole batch, and re-check two random chunks with the CPU oracle.
+Runs for --seconds; prints one JSON line (cases, mismatches with their seeds).
+
+    python tools/lab/stress.py --seconds 600
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seconds", type=float, default=300)
+    ap.add_argument("--seed", type=int, default=0)
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+
+    from fullsize_util import check_prove, check_verify, chunk_rows
+    from oracle import toploc_oracle as TO
+    from paper_2505_07291_b200 import api
+    from paper_2505_07291_b200.synth import synth_device
+    eng = api.engine()
+    rng = np.random.default_rng(args.seed)
+    t_end = time.time() + args.seconds
+    cases, bad, chunks = 0, [], 0
+    keys = ("idx", "bits", "proofs", "stats", "chunk_accept", "rollout_accept")
+    while time.time() < t_end:
+        seed = int(rng.integers(1 << 30))
+        r = np.random.default_rng(seed)
+        H = int(r.choice([128, 520, 1024, 1030, 2048, 5120, 8192]))
+        R = int(r.integers(1, 48))
+        T = r.integers(0, int(r.choice([40, 400, 3000])), size=R)
+        offs = np.concatenate([[0], np.cumsum(T)]).astype(np.int64)
+        n_rows = int(offs[-1])
+        if n_rows == 0 or n_rows * H > 2.5e9:
+            continue
+        dist = str(r.choice(["normal", "massive", "zeros", "ones", "fp8"]))
+        prv = synth_device(n_rows, H, seed, "normal" if dist == "fp8" else dist)
+        if dist == "fp8":
+            prv = prv.to(torch.float8_e4m3fn).to(torch.bfloat16)
+        mode = int(r.integers(3))
+        if mode == 0:
+            val = prv
+        elif mode == 1:
+            val = synth_device(n_rows, H, seed, "normal" if dist == "fp8" else dist, jitter_thr=3277,
+                               jitter_seed=seed + 1)
+        else:
+            val = synth_device(n_rows, H, seed + 7)
+        outs = []
+        for ctas in (-2, -1, 0):
+            plan = eng.plan(offs, H)
+            plan.select(prv.view(torch.int16), ctas_per_sm=ctas)
+            plan.commit()
+            plan.verify(val.view(torch.int16), ctas_per_sm=ctas)
+            torch.cuda.synchronize()
+            outs.append(plan)
+        for k in keys:
+            a = getattr(outs[0], k)
+            for o in outs[1:]:
+                if not torch.equal(a, getattr(o, k)):
+                    bad.append({"seed": seed, "what": f"{k} differs across launch shapes", "H": H, "R": R})
+                    break
+        plan = outs[0]
+        if plan.n_chunks:
+            table = chunk_rows(offs)
+            js = sorted(set(r.choice(plan.n_chunks, size=min(2, plan.n_chunks), replace=False).tolist()))
+            proofs, bp = check_prove(prv, table, js, plan.idx, plan.bits, plan.proofs)
+            st = plan.stats.cpu().numpy().view(api.STATS_DTYPE).reshape(-1)
+            bv, _ = check_verify(val, table, js, proofs, st, plan.chunk_accept.cpu().numpy(), TO.Thresholds())
+            if bp or bv:
+                bad.append({"seed": seed, "what": "oracle", "prove": bp, "verify": bv, "H": H, "R": R})
+            chunks += plan.n_chunks
+        cases += 1
+    print(json.dumps({"cases": cases, "chunks": chunks, "mismatches": bad[:20], "n_mismatches": len(bad)}))
+
+
+if __name__ == "__main__":
+    main()
