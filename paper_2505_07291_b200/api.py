@@ -43,12 +43,13 @@ class Thresholds:
     Defaults are measured (tools/calibrate_thresholds.py, profiles/r02_calibration.json):
     on a hidden-5120 Llama-shaped bf16 model, honest recomputations (prefill vs decode
     kernels, other batch shapes, the math attention backend, an fp32 model) reach at most
-    17 exponent mismatches, mean 2.84 and median 2 per chunk over 768 chunks each; the
-    defaults are those maxima x 1.5 + 2.  They reject every rollout of fp8-e4m3 weights,
-    weights perturbed by 1 % of their std, another model and one layer fewer (the paper's
-    values recalled in ``paper()`` accept 2 of 48 rollouts of the 1 % perturbation)."""
+    18 exponent mismatches, mean 2.84 and median 2 per chunk over 3072 chunks each; the
+    defaults are those maxima x 1.5 + 2, rounded up.  They reject every rollout of
+    fp8-e4m3 weights, weights perturbed by 1 % of their std, another model and one layer
+    fewer (as do the paper's values recalled in ``paper()``, which pass 88 % of the 1 %
+    perturbation's chunks and 43 of 48 rollouts of fp8-rounded activations, against 5)."""
 
-    max_exp_mismatch: int = 28
+    max_exp_mismatch: int = 29
     max_mant_mean: float = 7.0
     max_mant_median: float = 5.0
 

@@ -169,6 +169,7 @@ def main():
     out = {"model": f"random-init Llama, hidden {H}, {args.layers} layers, vocab 32000, bf16",
            "rollouts": B, "tokens_per_rollout": T, "chunks_per_scenario": int(B * T // 32),
            "defaults": dataclasses.asdict(api.Thresholds()),
+           "paper": dataclasses.asdict(api.Thresholds.paper()),
            "honest_maxima": hmax,
            "supported_thresholds": {"max_exp_mismatch": proposal.max_exp_mismatch,
                                     "max_mant_mean": proposal.max_mant_mean,
@@ -179,7 +180,8 @@ def main():
         out["scenarios"][k] = {
             "exp_mismatch": dist(st["exp_mismatch"]), "mant_mean": dist(st["mant_mean"]),
             "mant_median": dist(st["mant_median"]),
-            "accept_at_defaults": accept(st, api.Thresholds()), "accept_at_supported": accept(st, proposal)}
+            "accept_at_defaults": accept(st, api.Thresholds()), "accept_at_supported": accept(st, proposal),
+            "accept_at_paper": accept(st, api.Thresholds.paper())}
     print(json.dumps(out))
 
 
