@@ -1,10 +1,10 @@
-# the driver's round-end checks on one GPU: every GPU test, smoke(), the default bench line, the reference arm
+# the driver's round-end checks on one GPU: every GPU test, smoke(), the reference arm, then the default bench line
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r2_pytest_full.log 2>&1
 echo pytest=$?
 tail -3 gpurun_out/r2_pytest_full.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke.log 2>&1; echo smoke=$?; tail -1 gpurun_out/r2_smoke.log
-python bench.py --steps 20 --warmup 5 > gpurun_out/r2_bench_full.json 2> gpurun_out/r2_bench_full.err; echo bench=$?
 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r2_ref_full.json 2> gpurun_out/r2_ref_full.err; echo ref=$?
+python bench.py --steps 20 --warmup 5 > gpurun_out/r2_bench_full.json 2> gpurun_out/r2_bench_full.err; echo bench=$?
 python -c "
 import json
 b=json.load(open('gpurun_out/r2_bench_full.json')); r=json.load(open('gpurun_out/r2_ref_full.json'))
