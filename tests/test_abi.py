@@ -63,6 +63,32 @@ def test_argument_validation_before_device(lib):
     assert lib.tl_synth_bf16(None, 0, 4, 0, 0, 0, None, None, 0, 0, None) == _ffi.TL_EINVAL
 
 
+def test_workspace_and_pointer_checks_before_device(lib):
+    """Undersized or misaligned workspaces and missing buffers are rejected on the host.
+    The pointers are never dereferenced: every call returns before its first CUDA call."""
+    fake = 1 << 20                                    # 256-aligned, never touched
+    offs = (ctypes.c_int64 * 3)(0, 64, 128)
+    ro = ctypes.cast(offs, ctypes.c_void_p).value
+    need = int(lib.tl_workspace_bytes(2, 4, 128))
+    th = _ffi.Thresholds(38, 0, 10.0, 8.0)
+    E = _ffi.TL_EWORKSPACE
+    for ws, nbytes in ((fake, need - 1), (fake + 16, need), (fake, 0)):
+        assert lib.tl_select(fake, ro, 2, 128, 256, 32, 128, 4, fake, fake, ws, nbytes, None) == E
+        assert lib.tl_prove(fake, ro, 2, 128, 256, 32, 128, 4, fake, None, None, ws, nbytes, None) == E
+        assert lib.tl_verify(fake, ro, 2, 128, 256, 32, 128, 4, fake, ctypes.byref(th), None, None, None,
+                             ws, nbytes, None) == E
+    assert lib.tl_commit(fake, fake, 4, 128, fake, fake + 8, need, None) == E
+    # a missing buffer is EINVAL, whatever the workspace
+    assert lib.tl_select(fake, ro, 2, 128, 256, 32, 128, 4, None, fake, fake, need, None) == _ffi.TL_EINVAL
+    assert lib.tl_prove(fake, ro, 2, 128, 256, 32, 128, 4, None, None, None, fake, need, None) == _ffi.TL_EINVAL
+    assert lib.tl_verify(fake, ro, 2, 128, 256, 32, 128, 4, None, ctypes.byref(th), None, None, None,
+                         fake, need, None) == _ffi.TL_EINVAL
+    assert lib.tl_commit(None, fake, 4, 128, fake, fake, need, None) == _ffi.TL_EINVAL
+    # empty batches are no-ops that never look at the buffers
+    assert lib.tl_prove(None, None, 0, 0, 256, 32, 128, 0, None, None, None, None, 0, None) == _ffi.TL_OK
+    assert lib.tl_commit(None, None, 0, 128, None, None, 0, None) == _ffi.TL_OK
+
+
 def test_errors_map_to_python_exceptions(lib):
     with pytest.raises(ValueError):
         _ffi.check(_ffi.TL_EINVAL, "x")
