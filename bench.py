@@ -48,13 +48,22 @@ LAUNCHES_PER_STEP = 7      # select: prefix+select; commit: inv_table+commit; ve
 def launches_per_step(eng, hidden, plan, co_resident: bool) -> int:
     """Kernels one prove+verify step launches: 7 for large batches; a batch the ring grid
     covers (<= 256 rollouts) needs no chunk_prefix_kernel (select 1, verify 2), and a small
-    commitment on a prepared device is one launch (DESIGN 5.1b, 5.2)."""
+    commitment (<= 4 chunks per SM) is one commit_coop_kernel launch (DESIGN 5.1b, 5.2)."""
     import torch
     st = torch.cuda.current_stream(hidden.device).cuda_stream
     g = int(eng.lib.tl_ring_grid(hidden.data_ptr(), plan.H, plan.n_chunks, 0, 0, st))
     own_prefix = 0 < plan.n_chunks <= g and plan.n_roll <= 256
     small_commit = not co_resident and plan.n_chunks <= 4 * int(eng.lib.tl_stream_sms(st))
     return (1 if own_prefix else 2) + (1 if small_commit else 2) + (2 if own_prefix else 3)
+
+
+def select_kernel_name(eng, hidden, plan) -> str:
+    """The kernel tl_select launches for this batch (the roofline's dominant kernel)."""
+    import torch
+    st = torch.cuda.current_stream(hidden.device).cuda_stream
+    if int(eng.lib.tl_ring_grid(hidden.data_ptr(), plan.H, plan.n_chunks, 0, 0, st)) > 0:
+        return "ring_stream_kernel<0> (tl_select, TMA ring: one chunk per CTA)"
+    return "prove_select_kernel (tl_select)"
 
 
 def algorithmic_bytes_per_token(H: int) -> float:
@@ -692,7 +701,7 @@ def run_b200(args, cfg, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "config": config_block(args, cfg, R, R_total if shard is not None else world * R, world),
-            "roofline": {"bound": "hbm", "kernel": "prove_select_kernel (tl_select)", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": select_kernel_name(eng, prv, plan), "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": sel_bytes, "avg_launch_ms": kern_ms, "peak_source": peak_src,
                          "launch_timing": ("serial pass (in the timed schedule the kernel overlaps verify)"

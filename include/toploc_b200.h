@@ -132,10 +132,10 @@ int tl_select_ex(const uint16_t* hidden, const int64_t* row_off, int32_t n_roll,
 int tl_commit_ex(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int32_t K,
                  uint8_t* proofs_out, void* workspace, size_t workspace_bytes, int32_t co_resident,
                  void* stream);
-/* Build the GF(p) inverse tables on the current device and wait for them (once per
- * device; later calls return at once).  Optional: tl_commit builds them itself on first
- * use, but after tl_prepare a small batch's tl_commit is a single kernel launch.  Not
- * callable during stream capture (it synchronises). */
+/* Build the GF(p) inverse tables of the large-batch commitment on the current device and
+ * wait for them (once per device; later calls return at once).  Optional: tl_commit builds
+ * them itself on first use (a small batch's tl_commit -- at most 4 chunks per SM -- needs
+ * none).  Not callable during stream capture (it synchronises). */
 int tl_prepare(void);
 
 /* Grid of the TMA-ring kernel for this call shape (verify = 0: tl_select_ex, 1:

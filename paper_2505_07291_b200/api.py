@@ -612,8 +612,8 @@ class DualStreamPipeline(PartitionedPipeline):
         self.vstream = torch.cuda.Stream(eng.device)  # verify
         self.side = torch.cuda.Stream(eng.device)     # commit
         # a batch of at most one chunk per SM sub-partition leaves most SMs free: its
-        # commitment runs the 4-warp full-table kernel (one launch once the tables are
-        # prepared) instead of the co-resident form
+        # commitment runs the small-batch kernel (commit_coop_kernel, one launch, one CTA
+        # per chunk) instead of the co-resident form
         n_chunks = self.plans[0].n_chunks
         self.co_resident = n_chunks > 4 * int(eng.lib.tl_stream_sms(None))
         self.sms = None

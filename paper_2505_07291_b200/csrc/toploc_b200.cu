@@ -907,6 +907,36 @@ __device__ __forceinline__ uint32_t inv_of(const uint16_t* tab, uint32_t d, cons
   return m.pow(d, m.p - 2);
 }
 
+#ifndef TL_COMMIT_PROF
+#define TL_COMMIT_PROF 0
+#endif
+#if TL_COMMIT_PROF
+// Lab instrumentation (-DTL_COMMIT_PROF=1): clock64 cycles per commitment phase of global
+// warp 0 (0 table staging, 1 idx/bits load, 2 modulus, 3 divided differences,
+// 4 conversion, 5 serialise; 7 chunks), summed over launches; read by tl_commit_prof.
+__device__ unsigned long long g_cprof[8];
+__device__ long long g_cprof_last;
+#define CP_MARK(ph)                                                                   \
+  do {                                                                                \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                        \
+      const long long t_ = clock64();                                                 \
+      if ((ph) >= 0) g_cprof[(ph) < 0 ? 0 : (ph)] += (unsigned long long)(t_ - g_cprof_last); \
+      g_cprof_last = t_;                                                              \
+    }                                                                                 \
+  } while (0)
+#define CC_MARK(ph)                                                                   \
+  do {                                                                                \
+    const long long t_ = clock64();                                                   \
+    cc_acc_[ph] += t_ - cc_last_;                                                     \
+    cc_last_ = t_;                                                                    \
+    if ((ph) == 5 && blockIdx.x == 0 && threadIdx.x == 0)                             \
+      for (int i_ = 0; i_ < 6; ++i_) g_cprof[i_] += (unsigned long long)cc_acc_[i_];  \
+  } while (0)
+#else
+#define CP_MARK(ph) do {} while (0)
+#define CC_MARK(ph) do {} while (0)
+#endif
+
 // Newton divided differences, levels jl in [j0, j1) with j1 <= 32 (R0 + 1): the
 // register blocks r < R0 are complete (i < jl) and skipped at compile time; in
 // block R0 lanes with i < jl keep their value.  c[i] <- (c[i] - c[i-1]) / (x[i] - x[i-jl]).
@@ -962,6 +992,7 @@ __device__ __forceinline__ void interpolate_warp(const uint32_t (&x)[4], uint32_
   ndd_levels<MODE, 1, NU>(32, min(kk, 64), x, c, xs, m, tab, lane);
   ndd_levels<MODE, 2, NU>(64, min(kk, 96), x, c, xs, m, tab, lane);
   ndd_levels<MODE, 3, NU>(96, kk, x, c, xs, m, tab, lane);
+  CP_MARK(3);
   __syncwarp();  // every lane is done reading xs
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -977,6 +1008,7 @@ __device__ __forceinline__ void interpolate_warp(const uint32_t (&x)[4], uint32_
   conv_steps<1, CU>(kk - 33, max(kk - 64, 0), poly, xs, cs, m, lane);
   conv_steps<2, CU>(kk - 65, max(kk - 96, 0), poly, xs, cs, m, lane);
   conv_steps<3, CU>(kk - 97, 0, poly, xs, cs, m, lane);
+  CP_MARK(4);
 }
 
 // One warp commits one chunk: modulus search, GF(p) interpolation and the 258-byte
@@ -1040,6 +1072,7 @@ __device__ __forceinline__ void commit_chunk(const uint32_t (&raw)[4], const uin
     for (int b = lane; b < PB; b += 32) pr[b] = 0;
     return;
   }
+  CP_MARK(2);
   const ModP m(p);
   uint32_t x[4], c[4], poly[4];
 #pragma unroll
@@ -1066,6 +1099,7 @@ __device__ __forceinline__ void commit_chunk(const uint32_t (&raw)[4], const uin
     }
   }
   __syncwarp();
+  CP_MARK(5);
 }
 
 // ---- TMA bulk copy global -> shared with an mbarrier (the commitment's table staging)
@@ -1110,6 +1144,7 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
   // flight at once (a load loop over few warps would pay one L2 round trip per step,
   // ~16 us for a 4-warp CTA -- the small-batch commitment's largest cost)
   __shared__ __align__(8) uint64_t tab_bar;
+  CP_MARK(-1);
   if (threadIdx.x == 0) mbar_init(&tab_bar, 1);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1120,6 +1155,7 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
       bulk_copy_g2s(smem_raw + off, reinterpret_cast<const uint8_t*>(inv_tables) + off, kPiece, &tab_bar);
   }
   mbar_wait_parity(&tab_bar, 0);
+  CP_MARK(0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* xs = xs_all + warp * 128;
   uint32_t* cs = cs_all + warp * 128;
@@ -1143,6 +1179,10 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
       kk += __popc(__ballot_sync(0xFFFFFFFFu, iv >= 0));
     }
     TL_CHECK(j < n_chunks && kk <= K && K <= TL_MAX_K);
+    CP_MARK(1);
+#if TL_COMMIT_PROF
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_cprof[7] += 1;
+#endif
     // a small-batch CTA (one chunk per sub-partition) is latency-bound: unroll deeper so the
     // inverse lookups of later levels are issued ahead of the divided-difference chain
     commit_chunk<HALF ? kInvSmemHalf : kInvSmem, WARPS <= 4 ? 8 : kNddUnroll, WARPS <= 4 ? 4 : kConvUnroll>(
@@ -1152,6 +1192,205 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
 }
 
 
+// P(x) mod p for one point by Paterson-Stockmeyer over the zero-padded TL_MAX_K
+// coefficients (coef: 16-B aligned u16, shared memory) -- the residue of any exact
+// evaluation order (verify_tail_warp's, the oracle's).  2^32 mod p = -(p floor(2^32/p)).
+__device__ __forceinline__ uint32_t poly_eval_ps1(const uint16_t* coef, uint32_t x, const ModP& m) {
+  const uint32_t k32 = 0u - m.p * m.mu;
+  uint32_t xp[8];
+  xp[0] = 1u;
+  xp[1] = x;
+  xp[2] = m.mul(x, x);
+  xp[3] = m.mul(xp[2], x);
+  xp[4] = m.mul(xp[2], xp[2]);
+  xp[5] = m.mul(xp[4], x);
+  xp[6] = m.mul(xp[4], xp[2]);
+  xp[7] = m.mul(xp[4], xp[3]);
+  const uint32_t y = m.mul(xp[4], xp[4]);
+  const uint4* c8 = reinterpret_cast<const uint4*>(coef);
+  uint32_t acc = 0u;
+#pragma unroll 4
+  for (int kb = TL_MAX_K / 8 - 1; kb >= 0; --kb) {
+    const uint4 q = c8[kb];
+    const uint32_t cw[4] = {q.x, q.y, q.z, q.w};
+    unsigned long long s = 0ull;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s += (unsigned long long)((cw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu) * xp[e];
+    const uint32_t qk = m.red(m.red((uint32_t)s) + (uint32_t)(s >> 32) * k32);  // s < 2^35
+    acc = m.red(acc * y + qk);
+  }
+  return acc;
+}
+
+// tl_commit for small batches: one CTA per chunk.  The one-warp kernel above is a chain
+// of ~250 dependent steps (127 divided-difference levels, 127 Newton -> monomial steps),
+// ~14 us for a chunk whatever the batch.  Here the same polynomial -- the unique one of
+// degree < kk through the kk points, so the same coefficients -- comes from the Lagrange
+// form over a subproduct tree, with no inverse table and 2 x 7 levels:
+//   up:    M_node = M_left M_right, leaves X - x_t
+//   w_t  = y_t / M'(x_t)                                         (Paterson-Stockmeyer, Fermat)
+//   up:    V_node = V_left M_right + V_right M_left, leaves w_t  (root: sum_t w_t M / (X - x_t))
+// A level's 128 output coefficients take four threads each (strided partial sums of <= 33
+// products < p^2 in 64 bits, reduced, then summed over the quad).  Subproducts are stored
+// monic with their leading 1 (node n of degree d at [n (d + 1), (n + 1)(d + 1))), V nodes
+// with d coefficients.  The 128 - kk padding leaves are X with w = 0: the root's M and V
+// carry a factor X^(128 - kk), divided out by an index shift (c_k = V_{k + 128 - kk}).
+constexpr int kCoopCommitSub = 4;                                   // threads per coefficient
+constexpr int kCoopCommitThreads = TL_MAX_K * kCoopCommitSub;       // 512
+constexpr int kCoopLevels = 7;                                      // log2(TL_MAX_K)
+static_assert((1 << kCoopLevels) == TL_MAX_K, "tree levels");
+__device__ __forceinline__ uint32_t red64(unsigned long long s, const ModP& m, uint32_t k32) {  // s < 2^45
+  return m.red(m.red((uint32_t)s) + (uint32_t)(s >> 32) * k32);
+}
+__global__ void __launch_bounds__(kCoopCommitThreads)
+commit_coop_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits, int64_t n_chunks, int K,
+                   uint8_t* __restrict__ proofs) {
+  __shared__ uint32_t tm[kCoopLevels + 1][2 * TL_MAX_K];  // M levels (monic, leading 1 stored)
+  __shared__ uint32_t tv[2][TL_MAX_K];                    // V levels, ping-pong
+  __shared__ __align__(16) uint16_t dm[TL_MAX_K];         // M_kk'(X), zero-padded
+  __shared__ uint32_t hs[kHashSlots];
+  __shared__ uint32_t wmax[kCoopCommitThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int q = t >> 2, sub = t & (kCoopCommitSub - 1);  // coefficient / point q, quarter sub
+  const bool owner = sub == 0;                             // the point's own thread
+  const int64_t j = blockIdx.x;
+  if (j >= n_chunks) return;
+#if TL_COMMIT_PROF
+  long long cc_last_ = clock64(), cc_acc_[6] = {};
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_cprof[7] += 1;
+#endif
+  const int PB = 2 + 2 * K;
+  uint8_t* pr = proofs + j * PB;
+  const int32_t iv = owner && q < K ? idx[j * K + q] : -1;
+  const uint32_t yb = owner && q < K ? (uint32_t)bits[j * K + q] : 0u;
+  const uint32_t raw = (uint32_t)iv;
+  const unsigned mx = __reduce_max_sync(0xFFFFFFFFu, iv >= 0 ? raw : 0u);
+  if (lane == 0) wmax[warp] = mx;
+  const int kk = __syncthreads_count(iv >= 0);
+  TL_CHECK(kk >= 1 && kk <= K && K <= TL_MAX_K);
+  uint32_t maxidx = 0u;
+#pragma unroll
+  for (int w = 0; w < kCoopCommitThreads / 32; ++w) maxidx = max(maxidx, wmax[w]);
+  CC_MARK(0);
+
+  // ---- modulus: the largest prime with injective residues (as commit_chunk)
+  uint32_t p = kPMax;
+  if (maxidx >= kPMax) {
+    int pi = 0;
+    for (; pi < TL_N_PRIMES; ++pi) {
+      p = kPrimesDesc[pi];
+      const ModP mp(p);
+      if (t < kHashSlots) hs[t] = 0xFFFFFFFFu;
+      __syncthreads();
+      bool dup = false;
+      if (iv >= 0) {
+        const uint32_t v = mp.red(raw);
+        uint32_t h = (v * 0x9E3779B1u) >> (32 - kHashBits);
+        for (;;) {
+          const uint32_t old = atomicCAS(&hs[h], 0xFFFFFFFFu, v);
+          if (old == 0xFFFFFFFFu) break;
+          if (old == v) { dup = true; break; }
+          h = (h + 1) & (kHashSlots - 1);
+        }
+      }
+      if (!__syncthreads_or(dup)) break;
+    }
+    if (pi == TL_N_PRIMES) p = 0;
+  }
+  if (p == 0) {  // unprovable chunk: p = 0, zero coefficients
+    for (int b = t; b < PB; b += kCoopCommitThreads) pr[b] = 0;
+    return;
+  }
+  CC_MARK(1);
+  const ModP m(p);
+  const uint32_t k32 = 0u - m.p * m.mu;  // 2^32 mod p
+  const bool live = owner && q < kk;
+  const uint32_t x = live ? m.red(raw) : 0u;
+  const uint32_t y = live ? m.red(yb) : 0u;
+  const int pad = TL_MAX_K - kk;
+  if (owner) {  // leaf q: X - x_q (X for the padding points)
+    tm[0][2 * q] = x ? p - x : 0u;
+    tm[0][2 * q + 1] = 1u;
+  }
+  __syncthreads();
+
+  // ---- up the tree: M.  Output coefficient k < 2d of parent node n; the leading 1 by k = 0.
+#pragma unroll 1
+  for (int L = 0; L < kCoopLevels; ++L) {
+    const int d = 1 << L, n = q >> (L + 1), k = q & (2 * d - 1);
+    const uint32_t* A = tm[L] + 2 * n * (d + 1);  // children 2n, 2n + 1
+    const uint32_t* B = A + d + 1;
+    const int lo = k > d ? k - d : 0, hi = k < d ? k : d;
+    unsigned long long s0 = 0ull, s1 = 0ull;
+    int i = lo + sub;
+#pragma unroll 1
+    for (; i + kCoopCommitSub <= hi; i += 2 * kCoopCommitSub) {
+      s0 += (unsigned long long)A[i] * B[k - i];
+      s1 += (unsigned long long)A[i + kCoopCommitSub] * B[k - i - kCoopCommitSub];
+    }
+    if (i <= hi) s0 += (unsigned long long)A[i] * B[k - i];
+    uint32_t v = red64(s0 + s1, m, k32);
+    v += __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+    v = m.red(v + __shfl_xor_sync(0xFFFFFFFFu, v, 2));
+    uint32_t* P = tm[L + 1] + n * (2 * d + 1);
+    if (owner) {
+      P[k] = v;
+      if (k == 0) P[2 * d] = 1u;
+    }
+    __syncthreads();
+  }
+  CC_MARK(2);
+
+  // ---- w_q = y_q / M_kk'(x_q); M_kk(X) = M(X) / X^pad: m_k = M[k + pad], k <= kk
+  const uint32_t* Mr = tm[kCoopLevels];
+  if (owner) dm[q] = (uint16_t)(q < kk ? m.mul((uint32_t)(q + 1), Mr[q + 1 + pad]) : 0u);  // (k + 1) m_{k+1}
+  __syncthreads();
+  if (owner) {
+    uint32_t w = 0u;
+    if (live) {
+      const uint32_t den = poly_eval_ps1(dm, x, m);  // distinct x: nonzero
+      w = m.mul(y, m.pow(den, p - 2u));
+    }
+    tv[0][q] = w;
+  }
+  __syncthreads();
+  CC_MARK(3);
+
+  // ---- up the tree: V (parent = V_A M_B + V_B M_A; V of level L has d coefficients)
+  int cur = 0;
+#pragma unroll 1
+  for (int L = 0; L < kCoopLevels; ++L) {
+    const int d = 1 << L, n = q >> (L + 1), k = q & (2 * d - 1);
+    const uint32_t* MA = tm[L] + 2 * n * (d + 1);
+    const uint32_t* MB = MA + d + 1;
+    const uint32_t* VA = tv[cur] + 2 * n * d;
+    const uint32_t* VB = VA + d;
+    const int lo = k > d ? k - d : 0, hi = k < d - 1 ? k : d - 1;  // V_i, i < d; M_{k-i}, k - i <= d
+    unsigned long long s0 = 0ull, s1 = 0ull;
+#pragma unroll 2
+    for (int i = lo + sub; i <= hi; i += kCoopCommitSub) {
+      s0 += (unsigned long long)VA[i] * MB[k - i];
+      s1 += (unsigned long long)VB[i] * MA[k - i];
+    }
+    uint32_t v = red64(s0 + s1, m, k32);
+    v += __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+    v = m.red(v + __shfl_xor_sync(0xFFFFFFFFu, v, 2));
+    if (owner) tv[cur ^ 1][q] = v;
+    cur ^= 1;
+    __syncthreads();
+  }
+  CC_MARK(4);
+
+  // ---- serialise p, c_0..c_{K-1} big-endian; c_k = V_{k + pad}
+  uint16_t* pw = reinterpret_cast<uint16_t*>(pr);
+  if (t < K) {
+    const uint32_t c = t < kk ? tv[cur][t + pad] : 0u;
+    pw[1 + t] = (uint16_t)(((c & 0xFFu) << 8) | (c >> 8));
+  }
+  if (t == 0) pw[0] = (uint16_t)(((p & 0xFFu) << 8) | (p >> 8));
+  CC_MARK(5);
+}
+
 // One warp verifies one chunk from its ranked top-kk keys (top, shared memory): decode
 // the claimed coefficients (pword: this lane's big-endian u16 proof words t = lane + 32 q),
 // evaluate the polynomial at the kk indices (Horner, four points per lane), compare
@@ -1160,7 +1399,8 @@ commit_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits
 // scratch.
 constexpr int kPW = (TL_MAX_K + 1 + 31) / 32;  // proof words per lane
 #if TL_RING_STATS
-__device__ unsigned long long g_vt[8];  // lab: verify-tail phase cycles (decode, Horner, compare, median, write)
+__device__ unsigned long long g_vt[8];  // lab: verify-tail phase cycles (decode, Horner, compare, median, write),
+                                        // 5 entry -> first chunk ready, 6 entry -> first stage, 7 CTAs
 #endif
 // PS: evaluate by Paterson-Stockmeyer (shorter chains, ~40 registers more; the ring
 // finisher) instead of the two-half Horner (the one-warp kernel, 18 CTAs per SM).
@@ -1464,6 +1704,23 @@ __global__ void rollout_verdict_kernel(const uint8_t* __restrict__ chunk_accept,
 __device__ unsigned long long g_ring_stats[8];
 __device__ unsigned g_ring_trace[1024][4];  // CTA 0: per chunk theta magnitude, total, delta, kth magnitude
 __device__ unsigned g_ring_trace_n;
+// CTA 0's timeline of up to 64 launches (globaltimer ns): 0 entry, 1 roles start, 2 first
+// stages issued, 3 first stage landed, 4 chunk end (consumer 0), 5/6 cooperative finish
+// after its first / second barrier, 7 done
+__device__ unsigned long long g_ring_tl[64][32];  // 8 + 2t / 9 + 2t: consumer 0's stage t landed / scanned
+__device__ unsigned g_ring_tl_n;
+__device__ __forceinline__ unsigned long long ring_gt() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__shared__ unsigned g_ring_tl_launch;  // this launch's timeline row (CTA 0)
+#define RING_TL(slot)                                                                        \
+  do {                                                                                       \
+    if (blockIdx.x == 0) g_ring_tl[g_ring_tl_launch & 63u][(slot) & 31] = ring_gt();          \
+  } while (0)
+#else
+#define RING_TL(slot) do {} while (0)
 #endif
 constexpr int kRingConsumers = TL_RING_CONSUMERS;
 constexpr int kRingFinishers = TL_RING_FINISHERS;  // chunk c -> finisher c % kRingFinishers, buffer c & 1
@@ -1508,6 +1765,9 @@ struct RingSmem {
   unsigned long long theta_pub[2];  // by chunk parity: the largest threshold a consumer's compaction proved
   Spec spec;                      // the CTA's speculation state, updated in chunk order ...
   long long spec_seq;             // ... by the finisher of chunk spec_seq
+  alignas(16) unsigned coop_hist[128];  // cooperative finish (verify): |mantissa diff| histogram
+  unsigned coop_red[4];           // ... exponent mismatches, mantissa sum, matches
+  unsigned coop_p, coop_bad;      // ... the proof's modulus, not a prover prime
 };
 constexpr size_t kRingSmem = (sizeof(RingSmem) + 127) & ~(size_t)127;
 static_assert(kRingCtasPerSm * (kRingSmem + 1024) <= 228 * 1024, "ring CTAs per SM");
@@ -1684,9 +1944,14 @@ __device__ __forceinline__ void ring_produce(const SelArgs& a, RingSmem& S, int6
                                                                                  : (unsigned long long)n_chunks;
     const int bytes = 2 * g.n;
     const int nst = (bytes + kRingStageBytes - 1) / kRingStageBytes;
+    // the CTA's first chunk fills every free slot before the next chunk's lookup (a small
+    // batch has no next chunk, and its stages would otherwise wait for that lookup); later
+    // chunks issue one stage first, since the ring is full then
+    const int pre = t == 0 ? min(nst, kRingStages) : 1;  // lane 0's t
     if (lane == 0) {
       theta = *reinterpret_cast<volatile unsigned long long*>(&S.theta_next);  // the finishers' latest hint
-      issue(0, nst, bytes);
+      for (int q = 0; q < pre; ++q) issue(q, nst, bytes);
+      if (t == pre) RING_TL(2);
     }
     if (proofs && lane < 3)  // verify: the chunk's 258-byte proof into L2 for its finisher
       asm volatile("prefetch.global.L2 [%0];" ::"l"(proofs + j * (2 + 2 * a.K) + 128 * lane));
@@ -1694,16 +1959,226 @@ __device__ __forceinline__ void ring_produce(const SelArgs& a, RingSmem& S, int6
     const int64_t jn = (int64_t)gridDim.x + (int64_t)__shfl_sync(0xFFFFFFFFu, claim, 0);
     const ChunkGeo gn = warp_chunk_geo(a, jn < n_chunks ? jn : 0, lane);
     if (lane == 0)
-      for (int q = 1; q < nst; ++q) issue(q, nst, bytes);
+      for (int q = pre; q < nst; ++q) issue(q, nst, bytes);
     __syncwarp();
     j = jn;
     g = gn;
   }
 }
 
+// The ring kernel's outputs: select (idx, bits) or verify (proofs in; stats, verdicts out).
+struct RingOut {
+  int32_t* idx;
+  uint16_t* bits;
+  const uint8_t* proofs;
+  tl_thresholds th;
+  tl_chunk_stats* stats;
+  uint8_t* accept;
+};
+
+// Small batches: a CTA whose only chunk this is finishes it with its consumer warps and
+// its finisher together (kRingCoopThreads threads) instead of handing it to the one
+// finisher warp, whose single-warp tail (one bitonic sort of the union, four points per
+// lane for verify) is the latency of a batch of one chunk per CTA.
+//   - rank: candidate t (one per thread, the consumers' buffers concatenated) counts the
+//     candidates above it -- keys are distinct (the index is part of the key), so the
+//     count is its rank and sorted[rank] = key for rank < kk is the ranked top-kk;
+//   - select: the top-kk written by 128 threads;
+//   - verify: point i by thread i (poly_eval_ps1), counts by warp reductions, the
+//     mantissa median from a 128-bin histogram's prefix (the smallest t with more than q
+//     differences <= t, as select_rank in verify_tail_warp).
+// Returns false, having changed nothing, when the chunk needs the finisher's general path
+// (fewer than kk candidates: a re-scan; more candidates than threads); the caller then
+// continues its normal loop.
+constexpr int kRingCoopThreads = 32 * (kRingConsumers + 1);  // consumer warps + the finisher (warp kRingConsumers)
+constexpr int kRingCoopRankMax = 64;  // candidates per consumer buffer the cooperative finish ranks (typical: ~25)
+__device__ __forceinline__ void ring_coop_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kRingCoopThreads) : "memory");
+}
+template <bool VERIFY>
+__device__ bool ring_coop_finish(const SelArgs& a, RingSmem& S, const RingOut& o, int tid) {
+  static_assert(kRingFinishers == 1 && kRingConsumers * 32 + 32 == kRingCoopThreads, "coop layout");
+  if (VERIFY && tid >= 32 * kRingConsumers) {
+    // the finisher warp, idle while the consumers scan, decodes the proof of the CTA's only
+    // chunk (blockIdx.x): coefficients zero-padded to TL_MAX_K, modulus, prover-prime test
+    const int lane = tid & 31, K = a.K;
+    const uint16_t* pw = reinterpret_cast<const uint16_t*>(o.proofs + (int64_t)blockIdx.x * (2 + 2 * K));
+    unsigned p = 0u;
+#pragma unroll
+    for (int q = 0; q < kPW; ++q) {
+      const int t = lane + 32 * q;
+      if (t <= TL_MAX_K) {
+        const unsigned w = t <= K ? (unsigned)__ldg(pw + t) : 0u;
+        const unsigned v = ((w & 0xFFu) << 8) | (w >> 8);
+        if (t == 0) p = v;
+        else S.coef[0][t - 1] = (uint16_t)v;
+      }
+    }
+    if (lane == 0) {
+      S.coop_p = p;
+      S.coop_bad = prover_prime(p) ? 0u : 1u;
+    }
+#pragma unroll
+    for (int i = lane; i < 128; i += 32) S.coop_hist[i] = 0u;
+    if (lane < 4) S.coop_red[lane] = 0u;
+  }
+  ring_coop_bar();  // every consumer's count, flag, buffer and the job are visible
+#if TL_RING_STATS
+  const long long t0 = clock64();
+#endif
+  const RingJob job = S.job[0];
+  const int kk = job.kk, K = a.K, lane = tid & 31;
+  int total = 0, cmax = 0, ranked = 0, mq = -1, mi = 0;
+  int cq[kRingConsumers];
+  bool compacted = false;
+#pragma unroll
+  for (int q = 0; q < kRingConsumers; ++q) {
+    const int c = S.cnt[0][q];
+    cq[q] = c;
+    const int r = min(c, kk);  // a buffer's keys past its kk-th are not in the top-kk
+    if (tid >= ranked && tid < ranked + r) {
+      mq = q;
+      mi = tid - ranked;
+    }
+    ranked += r;
+    total += c;
+    cmax = max(cmax, c);
+    compacted = compacted || S.cmp[0][q];
+  }
+  if (tid == 0) RING_TL(5);
+  // uniform: the general path (fewer than kk candidates, an unranked buffer, too many to rank)
+  if (total < kk || cmax > kRingCoopRankMax || ranked > kRingCoopThreads) return false;
+  TL_CHECK(job.j >= 0 && kk >= 1 && kk <= K && K <= TL_MAX_K);
+  unsigned long long* sorted = S.uni[0];
+  if (mq >= 0) {
+    // rank = the keys above this one in every ranked buffer (its own included: keys are
+    // distinct, so its own buffer contributes its position), by branch-free binary searches
+    const unsigned long long key = S.wbuf[0][mq][mi];
+    int rank = 0;
+#pragma unroll
+    for (int q = 0; q < kRingConsumers; ++q) {
+      const unsigned long long* wb = S.wbuf[0][q];
+      int pos = 0;  // keys of buffer q above key: wb[0, pos) > key >= wb[pos]
+#pragma unroll
+      for (int step = kRingCoopRankMax / 2; step >= 1; step >>= 1)
+        if (pos + step <= cq[q] && wb[pos + step - 1] > key) pos += step;
+      if (pos + 1 <= cq[q] && wb[pos] > key) ++pos;  // cq = kRingCoopRankMax: the last step of a full search
+      rank += pos;
+    }
+    TL_CHECK(rank >= mi);
+    if (rank < kk) sorted[rank] = key;
+  }
+  const int64_t j = job.j;
+  TL_CHECK(j == (int64_t)blockIdx.x);
+  ring_coop_bar();  // sorted[0, kk) complete
+  if (tid == 0) RING_TL(6);
+  if (tid >= 32 * kRingConsumers) {  // the finisher warp: speculation, as ring_finish (no re-scan here)
+    Spec sp = S.spec;
+    int d = sp.delta;
+    if ((total > kk + TL_SPEC_HI || compacted) && d > 1) --d;
+    else if (total < kk + TL_SPEC_LO) ++d;
+    sp.delta = d;
+    sp.k0 = sp.k1;
+    sp.k1 = (unsigned)(sorted[kk - 1] >> 40);
+    spec_arm(sp);
+    spec_store(a.spec, blockIdx.x, sp, lane);
+  }
+  if (!VERIFY) {
+    if (tid < K) {
+      const unsigned long long key = sorted[tid < kk ? tid : 0];
+      o.idx[j * K + tid] = tid < kk ? (int32_t)key_idx(key) : -1;
+      o.bits[j * K + tid] = tid < kk ? (uint16_t)(key & 0xFFFFu) : (uint16_t)0;
+    }
+  } else {
+    const uint32_t p = S.coop_p;
+    const bool bad = S.coop_bad != 0u;
+    unsigned mism = 0u, msum = 0u, match = 0u;
+    if (!bad && tid < kk) {
+      const ModP m(p);
+      const unsigned long long key = sorted[tid];
+      const uint32_t claimed = poly_eval_ps1(S.coef[0], m.red(key_idx(key)), m);
+      const uint32_t obs = m.red((uint32_t)(key & 0xFFFFu));
+      if (((claimed >> 7) & 0xFFu) != ((obs >> 7) & 0xFFu)) {
+        mism = 1u;
+      } else {
+        const unsigned dd = (unsigned)abs((int)(claimed & 0x7Fu) - (int)(obs & 0x7Fu));
+        msum = dd;
+        match = 1u;
+        atomicAdd(&S.coop_hist[dd], 1u);
+      }
+    }
+    mism = __reduce_add_sync(0xFFFFFFFFu, mism);
+    msum = __reduce_add_sync(0xFFFFFFFFu, msum);
+    match = __reduce_add_sync(0xFFFFFFFFu, match);
+    if (lane == 0 && (mism | msum | match)) {
+      atomicAdd(&S.coop_red[0], mism);
+      atomicAdd(&S.coop_red[1], msum);
+      atomicAdd(&S.coop_red[2], match);
+    }
+    ring_coop_bar();  // counts and histogram complete
+    if (tid < 32) {
+      const unsigned nm = S.coop_red[2], ms = S.coop_red[1];
+      // the value of 0-based rank q: the smallest t with more than q differences <= t
+      const uint4 h = reinterpret_cast<const uint4*>(S.coop_hist)[lane];  // t = 4 lane + e
+      const unsigned c0 = h.x, c1 = c0 + h.y, c2 = c1 + h.z, c3 = c2 + h.w;
+      unsigned incl = c3;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+        if (lane >= off) incl += y;
+      }
+      const unsigned base = incl - c3;  // differences in t < 4 lane
+      auto value_of_rank = [&](unsigned q) {
+        const int e = base + c0 > q ? 0 : base + c1 > q ? 1 : base + c2 > q ? 2 : base + c3 > q ? 3 : 4;
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, e < 4);
+        const int l = bal ? __ffs(bal) - 1 : 31;
+        return 4 * l + __shfl_sync(0xFFFFFFFFu, e < 4 ? e : 3, l);
+      };
+      const unsigned q1 = nm ? (nm - 1) / 2 : 0, q2 = nm / 2;
+      const int v1 = value_of_rank(q1), v2 = value_of_rank(q2);
+      if (lane == 0) {
+        tl_chunk_stats st;
+        if (bad) {
+          st.exp_mismatch = (uint32_t)kk; st.n_match = 0; st.mant_sum = 0;
+          st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
+          st.mant_median = st.mant_mean;
+          st.flags = TL_STAT_BADPROOF;
+        } else {
+          st.exp_mismatch = S.coop_red[0]; st.n_match = nm; st.mant_sum = ms;
+          if (nm) {
+            st.mant_mean = (double)ms / (double)nm;
+            st.mant_median = ((double)v1 + (double)v2) * 0.5;
+          } else {
+            st.mant_mean = __longlong_as_double(0x7FF0000000000000ll);
+            st.mant_median = st.mant_mean;
+          }
+          const bool ok = (int)st.exp_mismatch <= o.th.max_exp_mismatch && st.mant_mean <= o.th.max_mant_mean &&
+                          st.mant_median <= o.th.max_mant_median;
+          st.flags = ok ? TL_STAT_ACCEPT : 0u;
+        }
+        if (o.stats) o.stats[j] = st;
+        o.accept[j] = (uint8_t)(st.flags & TL_STAT_ACCEPT);
+      }
+    }
+  }
+#if TL_RING_STATS
+  if (tid == 0) RING_TL(7);
+  if (tid == 0) {
+    atomicAdd(&g_ring_stats[0], 1ull);
+    atomicAdd(&g_ring_stats[1], (unsigned long long)total);
+    atomicAdd(&g_ring_stats[3], compacted ? 1ull : 0ull);
+    atomicAdd(&g_ring_stats[4], (unsigned long long)(clock64() - t0));
+  }
+#endif
+  return true;
+}
+
 // Consumer warp `wid`: scan its share of every stage; at each chunk end rank its buffer,
-// hand it to the chunk's finisher and continue with the next chunk.
-__device__ __forceinline__ void ring_consume(RingSmem& S, int K, int lane, int wid) {
+// hand it to the chunk's finisher and continue with the next chunk.  A CTA whose only
+// chunk this is (coop) finishes it cooperatively when ring_coop_finish applies.
+template <bool VERIFY>
+__device__ __forceinline__ void ring_consume(const SelArgs& a, RingSmem& S, int K, int lane, int wid, bool coop,
+                                             const RingOut& o, long long t_entry = 0) {
   RingScan w;
   w.theta = 0ull;
   w.cnt = 0;
@@ -1713,6 +2188,14 @@ __device__ __forceinline__ void ring_consume(RingSmem& S, int K, int lane, int w
   for (long long t = 0;; ++t) {
     const int s = (int)(t % kRingStages);
     mbar_wait_parity(&S.full[s], (unsigned)((t / kRingStages) & 1));
+#if TL_RING_STATS
+    if (t == 0 && wid == 0 && lane == 0) RING_TL(3);
+    if (t < 12 && wid == 0 && lane == 0) RING_TL(8 + 2 * t);
+    if (t == 0 && wid == 0 && lane == 0) {  // entry -> first stage landed; CTAs
+      atomicAdd(&g_vt[6], (unsigned long long)(clock64() - t_entry));
+      atomicAdd(&g_vt[7], 1ull);
+    }
+#endif
     const RingMeta m = S.meta[s];
     if (m.j < 0) break;
     const int kk = min(K, m.n);
@@ -1731,8 +2214,13 @@ __device__ __forceinline__ void ring_consume(RingSmem& S, int K, int lane, int w
 #endif
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.empty[s]);
+    if (t < 12 && wid == 0 && lane == 0) RING_TL(9 + 2 * t);
     if (m.q != m.nst - 1 || TL_RING_LAB == 2) continue;
     const int b = (int)(c & 1);
+    // the cooperative finish ranks by binary searches in the consumers' ranked buffers (the
+    // key set is unchanged; the general path gathers or ranks them again).  A fuller buffer
+    // (compactions, ties) sends the chunk to the general path, which does not need it ranked.
+    if (coop && w.cnt <= kRingCoopRankMax) ring_rank(w.wb, w.cnt, lane);
     if (lane == 0) {
       S.cnt[b][wid] = w.cnt;
       S.cmp[b][wid] = w.theta != theta0;
@@ -1740,6 +2228,8 @@ __device__ __forceinline__ void ring_consume(RingSmem& S, int K, int lane, int w
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.ready[b]);
+    if (wid == 0 && lane == 0) RING_TL(4);
+    if (coop && ring_coop_finish<VERIFY>(a, S, o, wid * 32 + lane)) return;
   }
   // no more chunks: release both finishers
   if (TL_RING_LAB == 2) c = -1;
@@ -1761,13 +2251,14 @@ template <bool VERIFY>
 __device__ __forceinline__ void ring_finish(const SelArgs& a, RingSmem& S, int f, int32_t* __restrict__ idx_out,
                                             uint16_t* __restrict__ bits_out, const uint8_t* __restrict__ proofs,
                                             const tl_thresholds& th, tl_chunk_stats* __restrict__ stats_out,
-                                            uint8_t* __restrict__ accept_out, int lane) {
+                                            uint8_t* __restrict__ accept_out, int lane, long long t_entry = 0) {
   const int K = a.K, PB = 2 + 2 * K;
   for (long long cseq = f;; cseq += kRingFinishers) {
     const int b = (int)(cseq & 1);  // the consumers' buffer parity of this chunk
     mbar_wait_parity(&S.ready[b], (unsigned)((cseq >> 1) & 1));
 #if TL_RING_STATS
     const long long t0 = clock64();
+    if (lane == 0 && cseq == f) atomicAdd(&g_vt[5], (unsigned long long)(t0 - t_entry));  // entry -> first chunk ready
 #endif
     const RingJob job = S.job[b];
     if (job.j < 0) break;
@@ -1954,6 +2445,16 @@ ring_stream_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restric
   extern __shared__ __align__(128) uint8_t ring_smem[];
   RingSmem& S = *reinterpret_cast<RingSmem*>(ring_smem);
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if TL_RING_STATS
+  const long long t_entry = clock64();
+  const unsigned long long tl_entry_ = ring_gt();
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    g_ring_tl_launch = atomicAdd(&g_ring_tl_n, 1u);
+    g_ring_tl[g_ring_tl_launch & 63u][0] = tl_entry_;
+  }
+#else
+  const long long t_entry = 0;
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRingStages; ++s) {
       mbar_init_count(&S.full[s], 1);
@@ -1998,10 +2499,18 @@ ring_stream_kernel(SelArgs a, int32_t* __restrict__ idx_out, uint16_t* __restric
   }
   __syncthreads();
   const int64_t n_chunks = min(a.n_chunks, a.prefix[a.n_roll]);
+  // one chunk per CTA (the grid covers the batch): the consumers and the finisher finish it together
+  const bool coop = TL_RING_LAB == 0 && (int64_t)gridDim.x >= n_chunks && (int64_t)blockIdx.x < n_chunks;
+  if (threadIdx.x == 0) RING_TL(1);
+  const RingOut o{idx_out, bits_out, proofs, th, stats_out, accept_out};
   if (wid == kRingProducer) ring_produce(a, S, n_chunks, lane, VERIFY ? proofs : nullptr);
-  else if (wid >= kRingConsumers)
-    ring_finish<VERIFY>(a, S, wid - kRingConsumers, idx_out, bits_out, proofs, th, stats_out, accept_out, lane);
-  else ring_consume(S, a.K, lane, wid);
+  else if (wid >= kRingConsumers) {
+    if (!(coop && ring_coop_finish<VERIFY>(a, S, o, (int)threadIdx.x)))
+      ring_finish<VERIFY>(a, S, wid - kRingConsumers, idx_out, bits_out, proofs, th, stats_out, accept_out, lane,
+                          t_entry);
+  } else {
+    ring_consume<VERIFY>(a, S, a.K, lane, wid, coop, o, t_entry);
+  }
 }
 
 // ----------------------------------------------------------------------------- record checks
@@ -2517,11 +3026,11 @@ int smem_attr_once(size_t bytes) {
   return TL_OK;
 }
 
-// The TMA-ring kernels take large batches of 16-B aligned chunks (H % 8 == 0 and an aligned
-// hidden pointer) when the caller leaves the launch shape to the library (ctas_per_sm == 0;
-// > 0 or < 0 selects the one-warp-per-chunk kernels, e.g. beside a co-resident commitment).
-constexpr int kRingMinRounds = 4;  // chunks per ring CTA, at least
-constexpr int kRingOptIn = -2;     // ctas_per_sm value that selects the ring kernels
+// The TMA-ring kernels take 16-B aligned chunks (H % 8 == 0 and an aligned hidden pointer):
+// small batches when the caller leaves the launch shape to the library (ctas_per_sm == 0),
+// any batch with -2; other values select the one-warp-per-chunk kernels (e.g. beside a
+// co-resident commitment).
+constexpr int kRingOptIn = -2;  // ctas_per_sm value that selects the ring kernels
 // A ring launch whose grid covers the batch (no chunk claims) over at most
 // kRingOwnPrefixMax rollouts builds its chunk prefix itself (no chunk_prefix_kernel).
 bool ring_own_prefix(int rg, int64_t n_chunks, int n_roll) {
@@ -2558,16 +3067,12 @@ int launch_commit_t(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, 
 
 // co_resident = 0: 32 warps, full 128 KiB table (fastest alone); 1: 8 warps, 64 KiB
 // half table, <= 64 registers -- fits beside 16 one-warp select/verify CTAs per SM.
-// A batch with at most one chunk per SM sub-partition runs 4-warp CTAs instead: every
-// chunk's warp then has a sub-partition to itself and the call is one chunk's latency
-// (a 32-warp CTA would stack 8 chunks on each sub-partition of a few SMs).
+// A batch with at most one chunk per SM sub-partition takes commit_coop_kernel (tl_commit_ex);
+// without it (co-resident callers), 4-warp CTAs: every chunk's warp has a sub-partition to
+// itself (a 32-warp CTA would stack 8 chunks on each sub-partition of a few SMs).
 constexpr int kSmallCommitWarps = 4;
 // Devices whose inverse tables are known built and visible to every stream (tl_prepare).
 std::atomic<uint32_t> g_tables_prepared{0u};
-bool tables_prepared() {
-  int dev = 0;
-  return cudaGetDevice(&dev) == cudaSuccess && (g_tables_prepared.load(std::memory_order_acquire) >> (dev & 31)) & 1u;
-}
 
 int launch_commit(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int K, uint8_t* proofs,
                   unsigned long long* next, int co_resident, cudaStream_t st) {
@@ -2692,10 +3197,12 @@ int tl_commit_ex(const int32_t* idx, const uint16_t* bits, int64_t n_chunks, int
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   unsigned long long* next = reinterpret_cast<unsigned long long*>(ws + L.next) + 1;  // commit's own counter
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // a small batch (one chunk per warp of the 4-warp grid) on a device whose tables are
-  // prepared is one launch: no table build, no chunk counter
-  if (!co_resident && n_chunks <= (int64_t)stream_sms(st) * kSmallCommitWarps && tables_prepared())
-    return launch_commit(idx, bits, n_chunks, K, proofs_out, nullptr, 0, st);
+  // a small batch (at most one chunk per SM sub-partition) is one launch of one 128-thread
+  // CTA per chunk: no inverse table, no chunk counter (commit_coop_kernel)
+  if (!co_resident && n_chunks <= (int64_t)stream_sms(st) * kSmallCommitWarps) {
+    commit_coop_kernel<<<(unsigned)n_chunks, kCoopCommitThreads, 0, st>>>(idx, bits, n_chunks, K, proofs_out);
+    return launch_status();
+  }
   inv_table_kernel<<<dim3(kInvTableBlocks, kInvTables), kInvTableThreads, 0, st>>>(next);
   return launch_commit(idx, bits, n_chunks, K, proofs_out, next, co_resident, st);
 }
@@ -2876,7 +3383,25 @@ int tl_prepare(void) {
   return TL_OK;
 }
 
+#if TL_COMMIT_PROF
+int tl_commit_prof(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_cprof, sizeof(g_cprof)) != cudaSuccess) return TL_ECUDA;
+  if (reset) {
+    static const unsigned long long z[8] = {};
+    if (cudaMemcpyToSymbol(g_cprof, z, sizeof(z)) != cudaSuccess) return TL_ECUDA;
+  }
+  return TL_OK;
+}
+#endif
 #if TL_RING_STATS
+int tl_ring_lab_timeline(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_ring_tl, sizeof(g_ring_tl)) != cudaSuccess) return TL_ECUDA;
+  if (reset) {
+    unsigned z = 0;
+    if (cudaMemcpyToSymbol(g_ring_tl_n, &z, 4) != cudaSuccess) return TL_ECUDA;
+  }
+  return TL_OK;
+}
 int tl_ring_lab_vt(unsigned long long* out) {
   static const unsigned long long z[8] = {};
   if (cudaMemcpyFromSymbol(out, g_vt, sizeof(g_vt)) != cudaSuccess) return TL_ECUDA;

@@ -192,10 +192,13 @@ def test_speculation_state_is_only_a_hint():
         assert np.all(st[:, 0] == 0) and np.all(st[:, 1] == K), name
 
 
-def test_prove_collisions_use_fallback_primes():
+@pytest.mark.parametrize("n", [60, 700])
+def test_prove_collisions_use_fallback_primes(n):
+    """60 chunks: the small-batch commitment (commit_coop_kernel); 700 (> 4 per SM): the
+    table-based one-warp commitment."""
     H = 5120
-    bits = synth_bits(0, 32 * 60, H, seed=5, dist=0)
-    _, proofs = check_prove_against_oracle(bits, [0, 32 * 60])
+    bits = synth_bits(0, 32 * n, H, seed=5, dist=0)
+    _, proofs = check_prove_against_oracle(bits, [0, 32 * n])
     assert any(int.from_bytes(p[:2], "big") != 65497 for p in proofs)
 
 
@@ -699,7 +702,8 @@ def test_pipeline_graph_matches_serial():
 def test_first_commits_on_two_streams_without_prepare_build_correct_tables():
     """The inverse tables are built by the first tl_commit when tl_prepare was not called.
     Two first calls racing on two streams of a fresh process must both produce the oracle's
-    proofs (the ready flag rises only when every table piece was written)."""
+    proofs (the ready flag rises only when every table piece was written).  640 chunks per
+    call: more than 4 per SM, so the table-based commitment (not commit_coop_kernel) runs."""
     import subprocess
     import sys
     code = r'''
@@ -708,8 +712,9 @@ from oracle import toploc_oracle as TO
 from oracle.synth_cpu import synth_bits
 from paper_2505_07291_b200 import _ffi
 L = _ffi.load()                       # no ToplocEngine: tl_prepare is never called
-H, T = 2048, 256
+H, T = 256, 32 * 640
 offs = np.array([0, T], dtype=np.int64)
+assert T // 32 > 4 * int(L.tl_stream_sms(None))
 outs = []
 streams = [torch.cuda.Stream(), torch.cuda.Stream()]
 bits = [synth_bits(0, T, H, seed=s, dist=1) for s in (1, 2)]
@@ -735,3 +740,26 @@ print("ok")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("H,lens,dist", [(5120, [700, 1, 33, 0, 64], 0), (3, [40, 7, 1], 1), (64, [1000, 1], 0),
+                                          (1024, [2048], 2), (8192, [300, 20], 3), (256, [129] * 9, 1)])
+def test_small_batch_commitment_kernels_agree(H, lens, dist):
+    """A small batch's commitment (commit_coop_kernel: Lagrange form over a subproduct tree)
+    and the co-resident one-warp kernel (Newton form, inverse tables) give the same proof
+    bytes for every chunk -- fallback primes (H 5120, 8192), chunks of fewer than K
+    elements (kk < 128: H 3, the one-row chunks), all-equal and tie-heavy values."""
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    bits = synth_bits(0, int(offs[-1]), H, seed=17, dist=dist)
+    eng = api.engine()
+    plan = eng.plan(offs, H)
+    assert plan.n_chunks <= 4 * int(eng.lib.tl_stream_sms(None))
+    plan.select(torch.from_numpy(bits.view(np.int16)).cuda())
+    plan.commit()
+    torch.cuda.synchronize()
+    coop = plan.proofs.clone()
+    plan.commit(co_resident=True)
+    torch.cuda.synchronize()
+    assert torch.equal(coop, plan.proofs)
+    got = [bytes(b) for b in coop.cpu().numpy()]
+    assert got == [p for r in TO.build_proofs(bits, offs) for p in r]

@@ -29,19 +29,29 @@ def ring_grid(h, H, n_chunks, ctas=RING, verify=1):
                                         torch.cuda.current_stream().cuda_stream))
 
 
+KEYS = ("idx", "bits", "proofs", "stats", "chunk_accept", "rollout_accept")
+
+
 def both_ways(h_prv, h_val, offs, H, th=api.Thresholds()):
     """Prove + verify with the ring kernels (ctas_per_sm = -2) and with the one-warp
-    kernels (-1); returns the two plans' host outputs."""
+    kernels (-1); returns the two plans' host outputs.  Each plan runs twice: the first
+    launches start from an untrained speculation state (every element a candidate), the
+    second from the trained one -- for a batch of one chunk per ring CTA the second takes
+    the cooperative finish (ring_coop_finish), the first its general path."""
     eng = api.engine()
     outs = []
     for ctas in (RING, -1):
         plan = eng.plan(offs, H)
-        plan.select(h_prv, ctas_per_sm=ctas)
-        plan.commit()
-        plan.verify(h_val, thresholds=th, ctas_per_sm=ctas)
-        torch.cuda.synchronize()
-        outs.append({k: getattr(plan, k).cpu().numpy() for k in
-                     ("idx", "bits", "proofs", "stats", "chunk_accept", "rollout_accept")})
+        runs = []
+        for _ in range(2):
+            plan.select(h_prv, ctas_per_sm=ctas)
+            plan.commit()
+            plan.verify(h_val, thresholds=th, ctas_per_sm=ctas)
+            torch.cuda.synchronize()
+            runs.append({k: getattr(plan, k).cpu().numpy() for k in KEYS})
+        for k in KEYS:
+            assert np.array_equal(runs[0][k], runs[1][k]), f"second launch differs in {k} (ctas {ctas})"
+        outs.append(runs[1])
         outs[-1]["plan"] = plan
     return outs
 
@@ -51,7 +61,7 @@ def check_case(prv, val, offs, H, th=api.Thresholds(), n_random=N_RANDOM):
     n_chunks = int(np.sum(-(-np.diff(offs) // 32)))
     assert ring_grid(prv, H, n_chunks) > 0, "the case must take the ring path"
     ring, warp = both_ways(prv.view(torch.int16), val.view(torch.int16), offs, H, th)
-    for k in ("idx", "bits", "proofs", "stats", "chunk_accept", "rollout_accept"):
+    for k in KEYS:
         assert np.array_equal(ring[k], warp[k]), f"ring vs one-warp kernels differ in {k}"
     plan = ring["plan"]
     table = chunk_rows(offs)
@@ -94,11 +104,13 @@ def test_ring_ragged_rollouts_with_partial_chunks():
     check_case(prv, val, offs, H)
 
 
+@pytest.mark.parametrize("R", [40, 2])
 @pytest.mark.parametrize("dist", ["zeros", "ones"])
-def test_ring_ties_across_consumer_warps(dist):
+def test_ring_ties_across_consumer_warps(dist, R):
     """All-equal chunks: the top-128 are the 128 lowest flat indices, all in the first
-    consumer warp's first tile; the other warps hold only losing ties."""
-    R, T, H = 40, 1024, 1024
+    consumer warp's first tile; the other warps hold only losing ties.  R = 2: one chunk
+    per ring CTA (cooperative finish, or its fallback when the ties overflow it)."""
+    T, H = 1024, 1024
     offs = np.arange(R + 1, dtype=np.int64) * T
     prv = synth_device(R * T, H, seed=1, dist=dist)
     ring = check_case(prv, prv, offs, H)
@@ -106,9 +118,10 @@ def test_ring_ties_across_consumer_warps(dist):
     assert np.all(idx == np.arange(128)[None, :])
 
 
+@pytest.mark.parametrize("R", [40, 3])
 @pytest.mark.parametrize("kind", ["fp8_ties", "ascending", "descending", "spikes", "alternating"])
-def test_ring_adversarial_orderings(kind):
-    R, T, H = 40, 1024, 1024
+def test_ring_adversarial_orderings(kind, R):
+    T, H = 1024, 1024
     C, n = 32, 32 * 1024
     offs = np.arange(R + 1, dtype=np.int64) * T
     dev = torch.device("cuda")
@@ -137,12 +150,14 @@ def test_ring_adversarial_orderings(kind):
     check_case(prv, val, offs, H)
 
 
+@pytest.mark.parametrize("R", [40, 2])
 @pytest.mark.parametrize("fill", ["garbage", "too_high", "zero"])
-def test_ring_speculation_state_is_only_a_hint(fill):
+def test_ring_speculation_state_is_only_a_hint(fill, R):
     """Workspace speculation slots pre-filled so that the first chunks start far too high
     (the ring re-scans them from global memory) or at zero (every element is a candidate,
-    the consumer warps compact): results stay bit-exact."""
-    R, T, H = 40, 1024, 5120
+    the consumer warps compact): results stay bit-exact.  R = 2 (64 chunks, one per ring
+    CTA): the cooperative finish hands both cases to the finisher's general path."""
+    T, H = 1024, 5120
     offs = np.arange(R + 1, dtype=np.int64) * T
     prv = synth_device(R * T, H, seed=8)
     val = synth_device(R * T, H, seed=8, jitter_thr=3277, jitter_seed=9)
@@ -170,7 +185,7 @@ def test_ring_speculation_state_is_only_a_hint(fill):
     ref.commit()
     ref.verify(val.view(torch.int16), ctas_per_sm=-1)
     torch.cuda.synchronize()
-    for k in ("idx", "bits", "proofs", "stats", "chunk_accept", "rollout_accept"):
+    for k in KEYS:
         assert torch.equal(getattr(plan, k), getattr(ref, k)), k
 
 
@@ -205,3 +220,49 @@ def test_ring_small_batch_over_many_tiny_rollouts():
     assert 256 < len(T) and 0 < n_chunks <= ring_grid(prv, H, n_chunks, ctas=0, verify=0)
     val = synth_device(int(offs[-1]), H, seed=41, jitter_thr=3277, jitter_seed=42)
     check_case(prv, val, offs, H)
+
+
+def test_ring_cooperative_verify_forged_and_short_chunks():
+    """One chunk per ring CTA (cooperative finish once the speculation is trained) with
+    chunks shorter than K (one row of hidden 64: kk = 64) and forged proofs: moduli 2, 97
+    and 32769 (bad proofs) and the right coefficients under another prover prime. Ring and
+    one-warp verify agree in every statistic and verdict, over two launches each."""
+    H = 64
+    offs = np.array([0, 993, 993 + 65], dtype=np.int64)
+    prv = synth_device(int(offs[-1]), H, seed=51)
+    val = synth_device(int(offs[-1]), H, seed=51, jitter_thr=3277, jitter_seed=52)
+    eng = api.engine()
+    ref = eng.plan(offs, H)
+    ref.select(prv.view(torch.int16), ctas_per_sm=-1)
+    ref.commit()
+    torch.cuda.synchronize()
+    n = ref.n_chunks
+    assert ring_grid(prv, H, n, ctas=0) >= n
+    forged = ref.proofs.clone().view(n, -1)
+    for c, p in ((0, 2), (1, 97), (2, 32769), (3, 65479)):
+        forged[c, 0], forged[c, 1] = p >> 8, p & 0xFF
+    forged[0, 2:] = 0
+    outs = {}
+    for ctas in (RING, -1):
+        plan = eng.plan(offs, H)
+        plan.select(prv.view(torch.int16), ctas_per_sm=ctas)   # trains the speculation
+        runs = []
+        for _ in range(2):
+            plan.verify(val.view(torch.int16), forged.view(-1), ctas_per_sm=ctas)
+            torch.cuda.synchronize()
+            runs.append({k: getattr(plan, k).cpu().numpy() for k in ("stats", "chunk_accept", "rollout_accept")})
+        for k in runs[0]:
+            assert np.array_equal(runs[0][k], runs[1][k]), k
+        outs[ctas] = runs[1]
+    for k in outs[RING]:
+        assert np.array_equal(outs[RING][k], outs[-1][k]), f"ring vs one-warp verify differ in {k}"
+    st = outs[RING]["stats"].view(api.STATS_DTYPE).reshape(-1)
+    assert all(st["flags"][c] & 2 for c in (0, 1, 2)) and not st["flags"][3] & 2
+    from oracle import toploc_oracle as TO
+    assert 65479 in TO.PRIME_SET
+    fp = forged.cpu().numpy()
+    th = api.Thresholds()
+    bad, _ = check_verify(val, chunk_rows(offs), list(range(n)), {j: bytes(fp[j]) for j in range(n)}, st,
+                          outs[RING]["chunk_accept"], TO.Thresholds(th.max_exp_mismatch, th.max_mant_mean,
+                                                                    th.max_mant_median))
+    assert not bad, bad[:8]

@@ -59,11 +59,24 @@ def main():
         outs = []
         for ctas in (-2, -1, 0):
             plan = eng.plan(offs, H)
-            plan.select(prv.view(torch.int16), ctas_per_sm=ctas)
-            plan.commit()
-            plan.verify(val.view(torch.int16), ctas_per_sm=ctas)
-            torch.cuda.synchronize()
+            first = None
+            for rep in range(2):  # the second launch starts from a trained speculation state
+                plan.select(prv.view(torch.int16), ctas_per_sm=ctas)
+                plan.commit()
+                plan.verify(val.view(torch.int16), ctas_per_sm=ctas)
+                torch.cuda.synchronize()
+                if rep == 0:
+                    first = {k: getattr(plan, k).clone() for k in keys}
+            for k in keys:
+                if not torch.equal(first[k], getattr(plan, k)):
+                    bad.append({"seed": seed, "what": f"{k} differs between launches (ctas {ctas})", "H": H, "R": R})
             outs.append(plan)
+        # the commitment's other kernel (co-resident form: the table-based one-warp kernel)
+        ref = outs[0].proofs.clone()
+        outs[0].commit(co_resident=True)
+        torch.cuda.synchronize()
+        if not torch.equal(ref, outs[0].proofs):
+            bad.append({"seed": seed, "what": "proofs differ between commitment kernels", "H": H, "R": R})
         for k in keys:
             a = getattr(outs[0], k)
             for o in outs[1:]:

@@ -32,6 +32,10 @@ def main():
     prv = synth_device(R * T, H, 1000, args.dist).view(torch.int16)
     val = synth_device(R * T, H, 1000, args.dist, jitter_thr=3277, jitter_seed=1001).view(torch.int16)
     out = {"shape": [R, T, H]}
+
+    def entry_us(vt):  # per CTA: kernel entry -> first ring stage landed / first chunk handed to the finisher
+        n = max(1, vt[7])
+        return {"first_stage": round(vt[6] / n / 1.9e3, 3), "first_ready": round(vt[5] / n / 1.9e3, 3)}
     plans = {}
     for mode in args.modes.split(","):
         ctas = {"ring": -2, "auto": 0, "warp": -1}[mode]
@@ -69,11 +73,13 @@ def main():
                                         "tail_us_per_chunk": buf[4] / n / 1.9e3}
             vt = (ctypes.c_ulonglong * 8)()
             eng.lib.tl_ring_lab_vt(vt)
+            out["select_entry_us"] = entry_us(vt)
             plan.verify(val, ctas_per_sm=ctas)
             torch.cuda.synchronize()
             lab(buf, 1)
             eng.lib.tl_ring_lab_vt(vt)
             out["verify_tail_phase_us"] = [round(vt[i] / max(1, buf[0]) / 1.9e3, 3) for i in range(5)]
+            out["verify_entry_us"] = entry_us(vt)
             n = max(1, buf[0])
             out["ring_stats_verify"] = {"chunks": buf[0], "candidates_per_chunk": buf[1] / n,
                                         "rescans_per_chunk": buf[2] / n, "compacting_warps_per_chunk": buf[3] / n,
