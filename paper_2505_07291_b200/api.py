@@ -360,20 +360,28 @@ class Plan:
 
     def verify(self, h: torch.Tensor, proofs: torch.Tensor | None = None,
                thresholds: Thresholds = Thresholds(), stream=None, ctas_per_sm: int = 0,
-               workspace: torch.Tensor | None = None) -> torch.Tensor:
+               workspace: torch.Tensor | None = None, rollout_out: torch.Tensor | None = None) -> torch.Tensor:
         """tl_verify; ``workspace`` (same size as ``ws``) lets a verify run concurrently
-        with this plan's select on another stream."""
+        with this plan's select on another stream; ``rollout_out`` (uint8, one per rollout)
+        receives the rollout verdicts instead of ``rollout_accept`` (the pipelines give every
+        batch its own, so no copy is needed to keep them)."""
         h = self._check_hidden(h)
         e = self.eng
         pr = self.proofs if proofs is None else proofs
         ws = self.ws if workspace is None else workspace
+        ra = self.rollout_accept
+        if rollout_out is not None:
+            if rollout_out.dtype != torch.uint8 or rollout_out.numel() != self.n_roll or \
+                    rollout_out.device != self.eng.device or not rollout_out.is_contiguous():
+                raise ValueError(f"rollout_out must be a contiguous uint8 tensor of {self.n_roll} on {self.eng.device}")
+            ra = rollout_out
         th = thresholds.to_c()
         _ffi.check(e.lib.tl_verify_ex(h.data_ptr(), self.offs_dev.data_ptr(), self.n_roll, self.n_rows, self.H,
                                       e.chunk, e.topk, self.n_chunks, pr.data_ptr(), ctypes.byref(th),
                                       self.stats.data_ptr(), self.chunk_accept.data_ptr(),
-                                      self.rollout_accept.data_ptr(), ws.data_ptr(), ws.numel(),
+                                      ra.data_ptr(), ws.data_ptr(), ws.numel(),
                                       ctas_per_sm, self._stream(stream)), "tl_verify")
-        return self.rollout_accept
+        return ra
 
 
 class StepGraph:
@@ -467,6 +475,7 @@ class Pipeline:
         self.side.wait_stream(caller)
         n = len(provers)
         out = []
+        outs = [torch.empty(self.plans[0].n_roll, dtype=torch.uint8, device=self.eng.device) for _ in range(n)]
         sel_done = [None] * n
         com_done = [None] * n
         for k in range(n + 1):
@@ -490,9 +499,7 @@ class Pipeline:
                 main.wait_event(com_done[k - 1])
                 if on_verify:
                     on_verify(k - 1, "start", main)
-                acc = pl.verify(validators[k - 1], None, thresholds, main, self.ctas)
-                with torch.cuda.stream(main):
-                    out.append(acc.clone())
+                out.append(pl.verify(validators[k - 1], None, thresholds, main, self.ctas, rollout_out=outs[k - 1]))
                 if on_verify:
                     on_verify(k - 1, "end", main)
                 if self.edge_on_main and k == n - 1:  # pipeline drain: the last commit on the main SMs
@@ -549,6 +556,7 @@ class PartitionedPipeline(Pipeline):
             st.wait_stream(caller)
         n = len(provers)
         out = []
+        outs = [torch.empty(self.plans[0].n_roll, dtype=torch.uint8, device=self.eng.device) for _ in range(n)]
         com_done = [None] * n
         ver_done = [None] * n
         for k in range(n + 2):
@@ -573,9 +581,8 @@ class PartitionedPipeline(Pipeline):
                 ver.wait_event(com_done[j])
                 if on_verify:
                     on_verify(j, "start", ver)
-                acc = pl.verify(validators[j], None, thresholds, ver, self.ctas, workspace=self.ws_verify[j % 3])
-                with torch.cuda.stream(ver):
-                    out.append(acc.clone())
+                out.append(pl.verify(validators[j], None, thresholds, ver, self.ctas, workspace=self.ws_verify[j % 3],
+                                     rollout_out=outs[j]))
                 if on_verify:
                     on_verify(j, "end", ver)
                 ver_done[j] = torch.cuda.Event()
