@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SUITES = ["tests/test_gpu_parity.py", "tests/test_gpu_ring.py"]
 SELECT = ("fuzz or split or ragged or many or malformed or forged or fails_closed or speculation or orderings or "
-          "ties or golden or shapes or variants or matches_warp or wide or other_chunk")
+          "ties or golden or shapes or variants or matches_warp or wide or other_chunk or commitment or cooperative")
 
 
 def test_fuzz_and_parity_suites_pass_under_the_checked_build():
