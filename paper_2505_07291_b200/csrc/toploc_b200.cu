@@ -1226,17 +1226,20 @@ __device__ __forceinline__ uint32_t poly_eval_ps1(const uint16_t* coef, uint32_t
 // of ~250 dependent steps (127 divided-difference levels, 127 Newton -> monomial steps),
 // ~14 us for a chunk whatever the batch.  Here the same polynomial -- the unique one of
 // degree < kk through the kk points, so the same coefficients -- comes from the Lagrange
-// form over a subproduct tree, with no inverse table and 2 x 7 levels:
-//   up:    M_node = M_left M_right, leaves X - x_t
-//   w_t  = y_t / M'(x_t)                                         (Paterson-Stockmeyer, Fermat)
-//   up:    V_node = V_left M_right + V_right M_left, leaves w_t  (root: sum_t w_t M / (X - x_t))
-// A level's 128 output coefficients take four threads each (strided partial sums of <= 33
-// products < p^2 in 64 bits, reduced, then summed over the quad).  Subproducts are stored
-// monic with their leading 1 (node n of degree d at [n (d + 1), (n + 1)(d + 1))), V nodes
-// with d coefficients.  The 128 - kk padding leaves are X with w = 0: the root's M and V
-// carry a factor X^(128 - kk), divided out by an index shift (c_k = V_{k + 128 - kk}).
-constexpr int kCoopCommitSub = 4;                                   // threads per coefficient
-constexpr int kCoopCommitThreads = TL_MAX_K * kCoopCommitSub;       // 512
+// form over a subproduct tree, with 7 levels of short sums:
+//   w_t  = y_t / prod_{j != t} (x_t - x_j)          (two partial products per point; the
+//                                                    inverse from the prepared table, else Fermat)
+//   up:    M_node = M_left M_right,                  leaves X - x_t
+//          V_node = V_left M_right + V_right M_left, leaves w_t  (root: sum_t w_t M / (X - x_t))
+// Both trees advance together, one barrier per level.  A level's 128 output coefficients
+// of each take kCoopCommitSub = 2 threads (strided partial sums of <= 33 products < p^2 in
+// 64 bits, reduced, then summed over the pair; 2 measured faster than 4 or 8: every level
+// pays a barrier, and wider CTAs pay more for it).  Subproducts are stored monic with their
+// leading 1 (node n of degree d at [n (d + 1), (n + 1)(d + 1))), V nodes with d
+// coefficients.  The 128 - kk padding leaves are X with w = 0: the root's V carries a factor
+// X^(128 - kk), divided out by an index shift (c_k = V_{k + 128 - kk}).
+constexpr int kCoopCommitSub = 2;                                   // threads per coefficient
+constexpr int kCoopCommitThreads = TL_MAX_K * kCoopCommitSub;       // 256
 constexpr int kCoopLevels = 7;                                      // log2(TL_MAX_K)
 static_assert((1 << kCoopLevels) == TL_MAX_K, "tree levels");
 __device__ __forceinline__ uint32_t red64(unsigned long long s, const ModP& m, uint32_t k32) {  // s < 2^45
@@ -1245,13 +1248,13 @@ __device__ __forceinline__ uint32_t red64(unsigned long long s, const ModP& m, u
 __global__ void __launch_bounds__(kCoopCommitThreads)
 commit_coop_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__ bits, int64_t n_chunks, int K,
                    uint8_t* __restrict__ proofs) {
-  __shared__ uint32_t tm[kCoopLevels + 1][2 * TL_MAX_K];  // M levels (monic, leading 1 stored)
-  __shared__ uint32_t tv[2][TL_MAX_K];                    // V levels, ping-pong
-  __shared__ __align__(16) uint16_t dm[TL_MAX_K];         // M_kk'(X), zero-padded
+  __shared__ uint32_t tm[2][2 * TL_MAX_K];  // M levels (monic, leading 1 stored), ping-pong
+  __shared__ uint32_t tv[2][TL_MAX_K];      // V levels, ping-pong
+  __shared__ __align__(16) uint32_t xs[TL_MAX_K];
   __shared__ uint32_t hs[kHashSlots];
   __shared__ uint32_t wmax[kCoopCommitThreads / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int q = t >> 2, sub = t & (kCoopCommitSub - 1);  // coefficient / point q, quarter sub
+  const int q = t / kCoopCommitSub, sub = t & (kCoopCommitSub - 1);  // coefficient / point q, part sub
   const bool owner = sub == 0;                             // the point's own thread
   const int64_t j = blockIdx.x;
   if (j >= n_chunks) return;
@@ -1259,6 +1262,7 @@ commit_coop_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__
   long long cc_last_ = clock64(), cc_acc_[6] = {};
   if (blockIdx.x == 0 && threadIdx.x == 0) g_cprof[7] += 1;
 #endif
+  const bool tables = *reinterpret_cast<volatile unsigned*>(&g_inv_ready) == kInvReady;  // in flight early
   const int PB = 2 + 2 * K;
   uint8_t* pr = proofs + j * PB;
   const int32_t iv = owner && q < K ? idx[j * K + q] : -1;
@@ -1275,8 +1279,8 @@ commit_coop_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__
 
   // ---- modulus: the largest prime with injective residues (as commit_chunk)
   uint32_t p = kPMax;
+  int pi = 0;
   if (maxidx >= kPMax) {
-    int pi = 0;
     for (; pi < TL_N_PRIMES; ++pi) {
       p = kPrimesDesc[pi];
       const ModP mp(p);
@@ -1304,84 +1308,88 @@ commit_coop_kernel(const int32_t* __restrict__ idx, const uint16_t* __restrict__
   CC_MARK(1);
   const ModP m(p);
   const uint32_t k32 = 0u - m.p * m.mu;  // 2^32 mod p
-  const bool live = owner && q < kk;
-  const uint32_t x = live ? m.red(raw) : 0u;
-  const uint32_t y = live ? m.red(yb) : 0u;
-  const int pad = TL_MAX_K - kk;
-  if (owner) {  // leaf q: X - x_q (X for the padding points)
-    tm[0][2 * q] = x ? p - x : 0u;
+  const bool live = q < kk;
+  const uint32_t x = live ? m.red(raw) : 0u;  // the point of thread q's quad (owner's registers)
+  if (owner) {
+    xs[q] = x;
+    tm[0][2 * q] = x ? p - x : 0u;  // leaf q: X - x_q (X for the padding points)
     tm[0][2 * q + 1] = 1u;
   }
   __syncthreads();
-
-  // ---- up the tree: M.  Output coefficient k < 2d of parent node n; the leading 1 by k = 0.
-#pragma unroll 1
-  for (int L = 0; L < kCoopLevels; ++L) {
-    const int d = 1 << L, n = q >> (L + 1), k = q & (2 * d - 1);
-    const uint32_t* A = tm[L] + 2 * n * (d + 1);  // children 2n, 2n + 1
-    const uint32_t* B = A + d + 1;
-    const int lo = k > d ? k - d : 0, hi = k < d ? k : d;
-    unsigned long long s0 = 0ull, s1 = 0ull;
-    int i = lo + sub;
-#pragma unroll 1
-    for (; i + kCoopCommitSub <= hi; i += 2 * kCoopCommitSub) {
-      s0 += (unsigned long long)A[i] * B[k - i];
-      s1 += (unsigned long long)A[i + kCoopCommitSub] * B[k - i - kCoopCommitSub];
-    }
-    if (i <= hi) s0 += (unsigned long long)A[i] * B[k - i];
-    uint32_t v = red64(s0 + s1, m, k32);
-    v += __shfl_xor_sync(0xFFFFFFFFu, v, 1);
-    v = m.red(v + __shfl_xor_sync(0xFFFFFFFFu, v, 2));
-    uint32_t* P = tm[L + 1] + n * (2 * d + 1);
-    if (owner) {
-      P[k] = v;
-      if (k == 0) P[2 * d] = 1u;
-    }
-    __syncthreads();
-  }
   CC_MARK(2);
 
-  // ---- w_q = y_q / M_kk'(x_q); M_kk(X) = M(X) / X^pad: m_k = M[k + pad], k <= kk
-  const uint32_t* Mr = tm[kCoopLevels];
-  if (owner) dm[q] = (uint16_t)(q < kk ? m.mul((uint32_t)(q + 1), Mr[q + 1 + pad]) : 0u);  // (k + 1) m_{k+1}
-  __syncthreads();
-  if (owner) {
-    uint32_t w = 0u;
-    if (live) {
-      const uint32_t den = poly_eval_ps1(dm, x, m);  // distinct x: nonzero
-      w = m.mul(y, m.pow(den, p - 2u));
+  // ---- w_q = y_q / prod_{j < kk, j != q} (x_q - x_j): q's threads take j = sub mod kCoopCommitSub
+  {
+    const uint32_t xq = xs[q];
+    uint32_t p0 = 1u, p1 = 1u;
+#pragma unroll 4
+    for (int i = 0; i < TL_MAX_K / (2 * kCoopCommitSub); ++i) {
+      const int j0 = 2 * kCoopCommitSub * i + sub, j1 = j0 + kCoopCommitSub;
+      const uint32_t d0 = (j0 == q || j0 >= kk) ? 1u : m.sub(xq, xs[j0]);
+      const uint32_t d1 = (j1 == q || j1 >= kk) ? 1u : m.sub(xq, xs[j1]);
+      p0 = m.mul(p0, d0);
+      p1 = m.mul(p1, d1);
     }
-    tv[0][q] = w;
+    uint32_t den = m.mul(p0, p1);
+#pragma unroll
+    for (int o = 1; o < kCoopCommitSub; o <<= 1) den = m.mul(den, __shfl_xor_sync(0xFFFFFFFFu, den, o));
+    // distinct x: den is nonzero
+    if (owner) {
+      uint32_t w = 0u;
+      if (live) {
+        const uint32_t inv = tables && pi < kInvTables ? (uint32_t)__ldg(g_inv_tables + (size_t)pi * 65536u + den)
+                                                      : m.pow(den, p - 2u);
+        w = m.mul(m.red(yb), inv);
+      }
+      tv[0][q] = w;
+    }
   }
   __syncthreads();
   CC_MARK(3);
 
-  // ---- up the tree: V (parent = V_A M_B + V_B M_A; V of level L has d coefficients)
+  // ---- up the trees.  Output coefficient k < 2d of parent node n (M: also its leading 1)
   int cur = 0;
 #pragma unroll 1
   for (int L = 0; L < kCoopLevels; ++L) {
     const int d = 1 << L, n = q >> (L + 1), k = q & (2 * d - 1);
-    const uint32_t* MA = tm[L] + 2 * n * (d + 1);
+    const uint32_t* MA = tm[cur] + 2 * n * (d + 1);  // children 2n, 2n + 1; M_A[d] = M_B[d] = 1
     const uint32_t* MB = MA + d + 1;
     const uint32_t* VA = tv[cur] + 2 * n * d;
     const uint32_t* VB = VA + d;
-    const int lo = k > d ? k - d : 0, hi = k < d - 1 ? k : d - 1;  // V_i, i < d; M_{k-i}, k - i <= d
-    unsigned long long s0 = 0ull, s1 = 0ull;
+    // M: sum_i A_i B_{k-i}, i in [max(0, k-d), min(k, d)];  V: sum_i VA_i MB_{k-i} + VB_i MA_{k-i},
+    // i in [max(0, k-d), min(k, d-1)]
+    const int lo = k > d ? k - d : 0, hm = k < d ? k : d, hv = k < d - 1 ? k : d - 1;
+    unsigned long long sm = 0ull, sv0 = 0ull, sv1 = 0ull;
 #pragma unroll 2
-    for (int i = lo + sub; i <= hi; i += kCoopCommitSub) {
-      s0 += (unsigned long long)VA[i] * MB[k - i];
-      s1 += (unsigned long long)VB[i] * MA[k - i];
+    for (int i = lo + sub; i <= hm; i += kCoopCommitSub) {
+      const uint32_t mb = MB[k - i], ma = MA[k - i];
+      sm += (unsigned long long)MA[i] * mb;
+      if (i <= hv) {
+        sv0 += (unsigned long long)VA[i] * mb;
+        sv1 += (unsigned long long)VB[i] * ma;
+      }
     }
-    uint32_t v = red64(s0 + s1, m, k32);
-    v += __shfl_xor_sync(0xFFFFFFFFu, v, 1);
-    v = m.red(v + __shfl_xor_sync(0xFFFFFFFFu, v, 2));
-    if (owner) tv[cur ^ 1][q] = v;
+    uint32_t vm = red64(sm, m, k32), vv = red64(sv0 + sv1, m, k32);
+#pragma unroll
+    for (int o = 1; o < kCoopCommitSub; o <<= 1) {  // sums of kCoopCommitSub values < p
+      vm += __shfl_xor_sync(0xFFFFFFFFu, vm, o);
+      vv += __shfl_xor_sync(0xFFFFFFFFu, vv, o);
+    }
+    vm = m.red(vm);
+    vv = m.red(vv);
+    if (owner) {
+      uint32_t* P = tm[cur ^ 1] + n * (2 * d + 1);
+      P[k] = vm;
+      if (k == 0) P[2 * d] = 1u;
+      tv[cur ^ 1][q] = vv;
+    }
     cur ^= 1;
     __syncthreads();
   }
   CC_MARK(4);
 
   // ---- serialise p, c_0..c_{K-1} big-endian; c_k = V_{k + pad}
+  const int pad = TL_MAX_K - kk;
   uint16_t* pw = reinterpret_cast<uint16_t*>(pr);
   if (t < K) {
     const uint32_t c = t < kk ? tv[cur][t + pad] : 0u;

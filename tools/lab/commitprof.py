@@ -28,7 +28,7 @@ lib.tl_commit_prof.restype = ctypes.c_int
 lib.tl_commit_prof.argtypes = [ctypes.c_void_p, ctypes.c_int]
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 names = ["staging", "load", "modulus", "ndd", "conversion", "serialise"]
-coop_names = ["load", "modulus", "m_tree", "weights", "v_tree", "serialise"]  # commit_coop_kernel
+coop_names = ["load", "modulus", "leaves", "weights", "trees", "serialise"]  # commit_coop_kernel
 out = {"lib": os.environ["TOPLOC_B200_LIB"]}
 for R, T, H in ((1, 32, 1024), (1, 2048, 1024), (1, 2048, 5120), (256, 8192, 5120)):
     h = synth.synth_device(R * T, H, 1000)
