@@ -266,3 +266,16 @@ def test_ring_cooperative_verify_forged_and_short_chunks():
                           outs[RING]["chunk_accept"], TO.Thresholds(th.max_exp_mismatch, th.max_mant_mean,
                                                                     th.max_mant_median))
     assert not bad, bad[:8]
+
+
+@pytest.mark.parametrize("H", [8, 16, 40])
+def test_ring_tiny_rows_and_short_chunks(H):
+    """Rows of 8-40 elements: every chunk holds fewer than K = 128 elements at H 8 (kk = the
+    chunk's element count), ragged rollouts leave one-row chunks; small batches (one chunk
+    per ring CTA), so the cooperative finish ranks and evaluates kk < 128 points."""
+    rng = np.random.default_rng(H)
+    T = rng.integers(1, 70, size=9)
+    offs = np.concatenate([[0], np.cumsum(T)]).astype(np.int64)
+    prv = synth_device(int(offs[-1]), H, seed=61)
+    val = synth_device(int(offs[-1]), H, seed=61, jitter_thr=3277, jitter_seed=62)
+    check_case(prv, val, offs, H)
