@@ -1988,15 +1988,19 @@ struct RingOut {
 // its finisher together (kRingCoopThreads threads) instead of handing it to the one
 // finisher warp, whose single-warp tail (one bitonic sort of the union, four points per
 // lane for verify) is the latency of a batch of one chunk per CTA.
-//   - rank: candidate t (one per thread, the consumers' buffers concatenated) counts the
-//     candidates above it -- keys are distinct (the index is part of the key), so the
-//     count is its rank and sorted[rank] = key for rank < kk is the ranked top-kk;
+//   - rank: each consumer has ranked its own buffer (ring_rank) before the barrier;
+//     candidate t (one per thread, the buffers' first kk keys concatenated) counts the keys
+//     above it in every buffer by binary search -- keys are distinct (the index is part of
+//     the key), so the count is its rank and sorted[rank] = key for rank < kk is the
+//     ranked top-kk;
 //   - select: the top-kk written by 128 threads;
-//   - verify: point i by thread i (poly_eval_ps1), counts by warp reductions, the
-//     mantissa median from a 128-bin histogram's prefix (the smallest t with more than q
-//     differences <= t, as select_rank in verify_tail_warp).
-// Returns false, having changed nothing, when the chunk needs the finisher's general path
-// (fewer than kk candidates: a re-scan; more candidates than threads); the caller then
+//   - verify: the finisher decodes the proof while the consumers scan; point i by thread i
+//     (poly_eval_ps1), counts by warp reductions, the mantissa median from a 128-bin
+//     histogram's prefix (the smallest t with more than q differences <= t, as
+//     select_rank in verify_tail_warp).
+// Returns false, having changed nothing the general path reads, when the chunk needs the
+// finisher's general path (fewer than kk candidates: a re-scan; a buffer over
+// kRingCoopRankMax keys, left unranked; more candidates than threads); the caller then
 // continues its normal loop.
 constexpr int kRingCoopThreads = 32 * (kRingConsumers + 1);  // consumer warps + the finisher (warp kRingConsumers)
 constexpr int kRingCoopRankMax = 64;  // candidates per consumer buffer the cooperative finish ranks (typical: ~25)
