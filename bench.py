@@ -555,7 +555,7 @@ def run_b200(args, cfg, rank, world, local_rank):
         sel_ms, com_ms, ver_ms = serial_ms["select"], serial_ms["commit"], serial_ms["verify"]
         accepted = int(outs[-1].sum().item())
         assert all(int(o.sum().item()) == accepted for o in outs)
-        spot_pipe = bool(torch.equal(pgraph_pipe.plans[(args.steps - 1) % 3].proofs, plan.proofs))
+        spot_pipe = bool(torch.equal(pgraph_pipe.plans[(args.steps - 1) % len(pgraph_pipe.plans)].proofs, plan.proofs))
         if spot is not None:
             spot["pipeline_proofs_equal_serial"] = spot_pipe
     else:

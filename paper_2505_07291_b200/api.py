@@ -551,19 +551,23 @@ class PartitionedPipeline(Pipeline):
     def run(self, provers, validators, thresholds: Thresholds = Thresholds(), on_verify=None,
             on_select=None, on_commit=None) -> list[torch.Tensor]:
         caller = torch.cuda.current_stream(self.eng.device)
-        sel, ver, side = self.main, self.vstream, self.side
-        for st in (sel, ver, side):
+        sels = getattr(self, "sstreams", None) or [self.main]
+        sides = getattr(self, "cstreams", None) or [self.side]
+        vers = getattr(self, "vstreams", None) or [self.vstream]
+        for st in (*sels, *sides, *vers):
             st.wait_stream(caller)
         n = len(provers)
+        nb = len(self.plans)  # rotating buffer sets
         out = []
         outs = [torch.empty(self.plans[0].n_roll, dtype=torch.uint8, device=self.eng.device) for _ in range(n)]
         com_done = [None] * n
         ver_done = [None] * n
         for k in range(n + 2):
             if k < n:
-                pl = self.plans[k % 3]
-                if k >= 3:
-                    sel.wait_event(com_done[k - 3])  # this plan's idx / bits consumed
+                pl = self.plans[k % nb]
+                sel, side = sels[k % len(sels)], sides[k % len(sides)]
+                if k >= nb:
+                    sel.wait_event(com_done[k - nb])  # this plan's idx / bits consumed
                 if on_select:
                     on_select(k, "start", sel)
                 pl.select(provers[k], sel, self.ctas)
@@ -572,22 +576,23 @@ class PartitionedPipeline(Pipeline):
                 done = torch.cuda.Event()
                 done.record(sel)
                 side.wait_event(done)
-                if k >= 3:
-                    side.wait_event(ver_done[k - 3])  # this plan's proofs read
+                if k >= nb:
+                    side.wait_event(ver_done[k - nb])  # this plan's proofs read
                 self._commit(pl, k, side, self.co_resident, on_commit, com_done)
             if k >= 2:
                 j = k - 2
-                pl = self.plans[j % 3]
+                pl = self.plans[j % nb]
+                ver = vers[j % len(vers)]
                 ver.wait_event(com_done[j])
                 if on_verify:
                     on_verify(j, "start", ver)
-                out.append(pl.verify(validators[j], None, thresholds, ver, self.ctas, workspace=self.ws_verify[j % 3],
+                out.append(pl.verify(validators[j], None, thresholds, ver, self.ctas, workspace=self.ws_verify[j % nb],
                                      rollout_out=outs[j]))
                 if on_verify:
                     on_verify(j, "end", ver)
                 ver_done[j] = torch.cuda.Event()
                 ver_done[j].record(ver)
-        for st in (sel, ver, side):
+        for st in (*sels, *sides, *vers):
             caller.wait_stream(st)
         return out
 
@@ -605,19 +610,33 @@ class PartitionedPipeline(Pipeline):
 
 class DualStreamPipeline(PartitionedPipeline):
     """The partitioned pipeline's schedule (select(k) and verify(k-2) on two streams,
-    commit(k-1) on a third, three rotating buffer sets) on ordinary streams of the whole
+    commit(k-1) on a third, rotating buffer sets) on ordinary streams of the whole
     GPU, with the co-resident commitment.  For small batches, whose kernels each use a
     fraction of the GPU, the three stages of different batches run concurrently; unlike
     green-context streams these can be captured in one CUDA graph (``PipelineGraph``)."""
 
-    def __init__(self, eng: "ToplocEngine", row_offsets, H: int, ctas_per_sm: int = 0):
+    def __init__(self, eng: "ToplocEngine", row_offsets, H: int, ctas_per_sm: int = 0,
+                 buffer_sets: int | None = None):
         Pipeline.__init__(self, eng, row_offsets, H, ctas_per_sm=ctas_per_sm)
-        self.plans.append(Plan(eng, row_offsets, H))
+        if buffer_sets is None:
+            # more sets put more batches in flight: worth it while a batch's kernels leave most
+            # SMs idle (configuration 1, 64 chunks: 0.0186 -> 0.0157 ms per step with 6), not
+            # once they fill the GPU (256 chunks at H 5120: 0.050 -> 0.057 ms)
+            buffer_sets = 6 if self.plans[0].n_chunks <= int(eng.lib.tl_stream_sms(None)) else 3
+        while len(self.plans) < max(3, buffer_sets):
+            self.plans.append(Plan(eng, row_offsets, H))
         self.ws_verify = [torch.empty_like(p.ws) for p in self.plans]
         self._handles = None
         self.main = torch.cuda.Stream(eng.device)     # select
         self.vstream = torch.cuda.Stream(eng.device)  # verify
         self.side = torch.cuda.Stream(eng.device)     # commit
+        # a small batch's kernels each use a fraction of the SMs: every stage alternates
+        # between two streams, so the same stage of consecutive batches can run at once
+        # (their plans, workspaces and verdict buffers are distinct: ``buffer_sets`` sets
+        # rotate, and the waits in run() order every reuse)
+        self.sstreams = [self.main, torch.cuda.Stream(eng.device)]
+        self.cstreams = [self.side, torch.cuda.Stream(eng.device)]
+        self.vstreams = [self.vstream, torch.cuda.Stream(eng.device)]
         # a batch of at most one chunk per SM sub-partition leaves most SMs free: its
         # commitment runs the small-batch kernel (commit_coop_kernel, one launch, one CTA
         # per chunk) instead of the co-resident form
