@@ -724,8 +724,11 @@ def run_b200(args, cfg, rank, world, local_rank):
                                        f"pipelined: commit(k) on a side stream overlaps verify(k-1); "
                                        f"select/verify {args.ctas} CTAs/SM" if args.pipeline_on else
                                        "graph: serial step replayed as one CUDA graph" if args.schedule == "graph"
-                                       else f"pipegraph: select, commit and verify of different batches on three "
-                                            f"streams, all {args.steps} batches captured as one CUDA graph"
+                                       else f"pipegraph: select, commit and verify of different batches, each stage "
+                                            f"alternating between {len(pgraph_pipe.sstreams)} streams, "
+                                            f"{len(pgraph_pipe.plans)} rotating buffer sets, all {args.steps} batches "
+                                            f"captured as one CUDA graph, uploaded before the timed region: "
+                                            f"{pgraph.uploaded}"
                                        if args.schedule == "pipegraph"
                                        else "serial")},
             "cpu_baseline": cpu,

@@ -384,6 +384,21 @@ class Plan:
         return ra
 
 
+def _upload_graph(graph: "torch.cuda.CUDAGraph", device) -> bool:
+    """Upload an instantiated graph to the device without running it (cuGraphUpload), so its
+    first replay does not pay the upload (~1 ms for a graph of 200 pipelined batches).
+    Returns False when the driver bindings are unavailable (the first replay uploads it)."""
+    try:
+        from cuda.bindings import driver
+        ex = graph.raw_cuda_graph_exec()
+        st = torch.cuda.current_stream(device).cuda_stream
+        err, = driver.cuGraphUpload(driver.CUgraphExec(ex), driver.CUstream(st))
+        torch.cuda.synchronize(device)
+        return err == driver.CUresult.CUDA_SUCCESS
+    except Exception:
+        return False
+
+
 class StepGraph:
     """One prove + verify step of a ``Plan`` captured as a CUDA graph (select, commit,
     verify and their small kernels: 7 launches replayed as one).  The captured tensors
@@ -436,6 +451,7 @@ class PipelineGraph:
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self.out = pipe.run(provers, validators, thresholds)
+        self.uploaded = _upload_graph(self.graph, dev)
 
     def replay(self) -> list[torch.Tensor]:
         self.graph.replay()
@@ -616,13 +632,17 @@ class DualStreamPipeline(PartitionedPipeline):
     green-context streams these can be captured in one CUDA graph (``PipelineGraph``)."""
 
     def __init__(self, eng: "ToplocEngine", row_offsets, H: int, ctas_per_sm: int = 0,
-                 buffer_sets: int | None = None):
+                 buffer_sets: int | None = None, streams_per_stage: int | None = None):
         Pipeline.__init__(self, eng, row_offsets, H, ctas_per_sm=ctas_per_sm)
+        # more buffer sets and streams put more batches in flight: worth it while a batch's
+        # kernels leave most SMs idle (configuration 1, 64 chunks, per step: 3 sets x 1 stream
+        # 14.3 us, 6 x 2 8.3 us, 12 x 4 6.5 us; tools/lab/pipegraph_sweep.py), not once they
+        # fill the GPU (256 chunks at H 5120: 3 x 2 41.9 us, 6 x 2 42.6, 3 x 3 46.4)
+        small = self.plans[0].n_chunks <= int(eng.lib.tl_stream_sms(None))
         if buffer_sets is None:
-            # more sets put more batches in flight: worth it while a batch's kernels leave most
-            # SMs idle (configuration 1, 64 chunks: 0.0186 -> 0.0157 ms per step with 6), not
-            # once they fill the GPU (256 chunks at H 5120: 0.050 -> 0.057 ms)
-            buffer_sets = 6 if self.plans[0].n_chunks <= int(eng.lib.tl_stream_sms(None)) else 3
+            buffer_sets = 12 if small else 3
+        if streams_per_stage is None:
+            streams_per_stage = 4 if small else 2
         while len(self.plans) < max(3, buffer_sets):
             self.plans.append(Plan(eng, row_offsets, H))
         self.ws_verify = [torch.empty_like(p.ws) for p in self.plans]
@@ -634,9 +654,10 @@ class DualStreamPipeline(PartitionedPipeline):
         # between two streams, so the same stage of consecutive batches can run at once
         # (their plans, workspaces and verdict buffers are distinct: ``buffer_sets`` sets
         # rotate, and the waits in run() order every reuse)
-        self.sstreams = [self.main, torch.cuda.Stream(eng.device)]
-        self.cstreams = [self.side, torch.cuda.Stream(eng.device)]
-        self.vstreams = [self.vstream, torch.cuda.Stream(eng.device)]
+        more = max(0, streams_per_stage - 1)
+        self.sstreams = [self.main] + [torch.cuda.Stream(eng.device) for _ in range(more)]
+        self.cstreams = [self.side] + [torch.cuda.Stream(eng.device) for _ in range(more)]
+        self.vstreams = [self.vstream] + [torch.cuda.Stream(eng.device) for _ in range(more)]
         # a batch of at most one chunk per SM sub-partition leaves most SMs free: its
         # commitment runs the small-batch kernel (commit_coop_kernel, one launch, one CTA
         # per chunk) instead of the co-resident form
