@@ -36,12 +36,12 @@ CHUNK, TOPK = 32, 128
 PROOF_BYTES = 2 + 2 * TOPK
 JITTER_THR = 3277          # 5 % of elements +-1 ulp in the validator's recompute
 # --schedule auto: the partitioned pipeline from this many chunks per GPU; below it the
-# three-stream pipeline captured as one CUDA graph (small batches: every kernel is
-# latency-bound and the stages of different batches overlap).  Measured ms per step,
-# pipegraph / graph / partition: configuration 1 (64 chunks, H 1024) 0.047 / 0.066 / 0.115;
-# H 5120 at 256 chunks 0.078 / 0.113 / 0.118, 1024 chunks 0.146 / 0.208 / 0.161, 2048 chunks
-# 0.268 / - / 0.257, 4096 chunks 0.431 / 0.554 / 0.432.
-AUTO_PIPELINE_MIN_CHUNKS = 2048
+# pipelined schedule captured as one CUDA graph (small batches: every kernel is
+# latency-bound and the stages of different batches overlap).  Measured ms per step at
+# H 5120 (pipegraph / partition, after the graph upload and the wider small-batch
+# schedule): 1024 chunks 0.116 / 0.157, 2048 0.206 / 0.240, 4096 0.396 / 0.402,
+# 8192 0.790 / 0.748; configuration 1 (64 chunks, H 1024) 0.009 / 0.115.
+AUTO_PIPELINE_MIN_CHUNKS = 8192
 LAUNCHES_PER_STEP = 7      # select: prefix+select; commit: inv_table+commit; verify: prefix+verify+verdict
 
 
@@ -782,7 +782,7 @@ def main():
     ap.add_argument("--spot-chunks", type=int, default=64, help="random chunks in the full-size parity check")
     ap.add_argument("--schedule", default="auto",
                     choices=["auto", "partition", "pipeline", "serial", "graph", "pipegraph"],
-                    help="auto (default): partition from 2048 chunks per GPU (AUTO_PIPELINE_MIN_CHUNKS), pipegraph below; "
+                    help="auto (default): partition from 8192 chunks per GPU (AUTO_PIPELINE_MIN_CHUNKS), pipegraph below; "
                          "partition: the pipeline on two SM partitions (green contexts), commit on "
                          "--commit-sms SMs, select/verify on the rest; "
                          "pipeline: commit(k) on a side stream, co-resident with verify(k-1) and select(k+1); "
