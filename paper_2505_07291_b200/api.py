@@ -423,6 +423,7 @@ class StepGraph:
             plan.select(prover)
             plan.commit()
             plan.verify(validator, None, thresholds)
+        self.uploaded = _upload_graph(self.graph, dev)
 
     def replay(self) -> torch.Tensor:
         self.graph.replay()

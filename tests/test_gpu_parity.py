@@ -479,6 +479,7 @@ def test_step_graph_matches_eager():
     torch.cuda.synchronize()
     want_p, want_s, want_a = plan.proofs.clone(), plan.stats.clone(), plan.rollout_accept.clone()
     g = api.StepGraph(plan, prv, val)
+    assert g.uploaded  # cuGraphUpload at construction: the first replay does not upload
     for _ in range(3):
         plan.proofs.zero_()
         plan.stats.zero_()
@@ -685,7 +686,9 @@ def test_pipeline_graph_matches_serial():
         plan.commit()
         want.append(plan.verify(val[k]).clone())
     pipe = api.DualStreamPipeline(eng, offs, H)
+    assert len(pipe.plans) == 12 and len(pipe.vstreams) == 4  # 3 chunks: the small-batch shape
     pg = api.PipelineGraph(pipe, prv, val)
+    assert pg.uploaded
     for _ in range(2):
         got = pg.replay()
         torch.cuda.synchronize()
